@@ -1,0 +1,145 @@
+/*
+ * lfmmi.h — C-ABI of the B200-native LF-MMI hot path (libpaper_lfmmi.so).
+ *
+ * Plain pointers and sizes only: no torch, no C++ types.  Every device
+ * pointer is a CUDA global-memory address on the current device; `stream`
+ * is a cudaStream_t passed as void*.  Entry points return LFMMI_OK (0) or a
+ * nonzero status; lfmmi_last_error() returns a thread-local message.
+ *
+ * Reference interfaces replaced (chainloss 0.1.0, /root/reference/pkg/src/chainloss):
+ *   lfmmi_graphs_create      graph.py:216-301   ChainGraphBatch._build (+ device residency)
+ *   lfmmi_forward_backward   forward_backward.py:290-307  forward_backward (fused, no trellis)
+ *   lfmmi_chain_loss         loss.py:42-84      chain_loss (num + den + combination)
+ *   lfmmi_forward_kernel     _kernels.py:54-122   forward_kernel   (parity/debug seam)
+ *   lfmmi_backward_kernel    _kernels.py:125-191  backward_kernel  (parity/debug seam)
+ *   lfmmi_posterior_kernel   _kernels.py:194-224  posterior_kernel (parity/debug seam)
+ *
+ * Semantics are those of the reference: scaled probability-
+ * space recursion with leaky HMM, finals applied at each item's own last
+ * frame, per-item numerical failure reported as data (fail frame >= 0, NaN
+ * log-probability, zero posterior rows), never as an error status.
+ */
+#ifndef LFMMI_H_
+#define LFMMI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFMMI_OK 0
+#define LFMMI_ERR_INVALID 1     /* bad argument / shape (reference: ValueError) */
+#define LFMMI_ERR_CUDA 2        /* CUDA runtime error */
+#define LFMMI_ERR_UNSUPPORTED 3 /* graph too large for the on-chip path, etc. */
+
+#define LFMMI_F32 0
+#define LFMMI_F64 1
+
+#define LFMMI_POST_WRITE 0    /* posteriors[b,t,:]  = gamma                     */
+#define LFMMI_POST_SUBTRACT 1 /* posteriors[b,t,:] -= gamma  (grad = num - den) */
+
+typedef struct lfmmi_graphs lfmmi_graphs;
+
+/* Message describing the last nonzero status returned on this thread. */
+const char *lfmmi_last_error(void);
+
+/* Library version string. */
+const char *lfmmi_version(void);
+
+/*
+ * Build a device-resident graph batch from the reference's padded host
+ * layout (graph.py:253-279).  G physical rows; row r has row_num_states[r]
+ * states and row_num_arcs[r] arcs.  Arrays are (G, max_arcs) in the
+ * from-state-sorted ("forward_*") layout and, optionally, the to-state-sorted
+ * ("backward_*") layout.  If the backward arrays are NULL they are derived by
+ * a stable sort.  final_probs is (G, max_states), initial_states is (G).
+ * Graph data is uploaded once (synchronously) and stays resident until
+ * lfmmi_graphs_destroy.
+ */
+int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t max_arcs, int32_t num_pdfs,
+                        const int64_t *row_num_states, const int64_t *row_num_arcs,
+                        const uint32_t *fw_from, const uint32_t *fw_to, const uint32_t *fw_pdf,
+                        const double *fw_prob, const uint32_t *bw_from, const uint32_t *bw_to,
+                        const uint32_t *bw_pdf, const double *bw_prob, const double *final_probs,
+                        const uint32_t *initial_states, lfmmi_graphs **out);
+
+int lfmmi_graphs_destroy(lfmmi_graphs *graphs);
+
+/* Shape queries on a graph handle. */
+int lfmmi_graphs_info(const lfmmi_graphs *graphs, int32_t *num_rows, int32_t *max_states,
+                      int32_t *max_arcs, int32_t *num_pdfs);
+
+/*
+ * Bytes of caller-provided device workspace needed by lfmmi_forward_backward
+ * / lfmmi_chain_loss for a batch of `total_frames` = sum of lengths over
+ * graph batches whose largest state count is `max_states`.
+ */
+size_t lfmmi_workspace_size(int32_t max_states, int64_t total_frames, int32_t precision);
+
+/*
+ * Fused forward-backward + posteriors for one graph batch (one launch).
+ *   row_map      (B)        int64  item -> physical graph row      [device]
+ *   loglikes     (B,T,D)    f32/f64 network outputs (log domain)   [device]
+ *   lengths      (B)        int32  valid frames per item (>= 1)    [device]
+ *   leak_pi      (G,S_max)  f32/f64 custom leak distribution, or NULL for uniform 1/S_g
+ *   workspace    device scratch of >= lfmmi_workspace_size(...) bytes
+ *   posteriors   (B,T,D)    f32/f64  written per `post_mode`; padded rows and failed
+ *                           items are zeroed (WRITE) / set to zero (SUBTRACT)
+ *   other_fail   (B) int32 or NULL: items whose other-graph recursion failed get
+ *                zero rows (used for the denominator pass of chain_loss)
+ *   log_probs    (B) f64 out (NaN when failed); fail_frames (B) int32 out (-1 or frame)
+ *   scale_logs   (B,T) f64 out or NULL
+ * precision selects f32 (LFMMI_F32) or f64 (LFMMI_F64) for all real arrays.
+ */
+int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t *row_map, int32_t batch,
+                           int32_t max_frames, int32_t num_pdfs, int32_t precision,
+                           const void *loglikes, const int32_t *lengths, double leak,
+                           double scale_floor, const void *leak_pi, void *workspace,
+                           size_t workspace_bytes, void *posteriors, int32_t post_mode,
+                           const int32_t *other_fail, double *log_probs, int32_t *fail_frames,
+                           double *scale_logs, void *stream);
+
+/*
+ * LF-MMI objective and gradient for one batch (loss.py:42-84): numerator pass
+ * (WRITE) then denominator pass (SUBTRACT) into `grad`, then a reduction of
+ * totals[0] = sum_ok(num_lp - den_lp), totals[1] = sum_ok(T_b),
+ * totals[2] = #failed   (device f64[3]; sum-reducible across ranks).
+ */
+int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *num_row_map,
+                     const lfmmi_graphs *denominator, const int64_t *den_row_map, int32_t batch,
+                     int32_t max_frames, int32_t num_pdfs, int32_t precision,
+                     const void *loglikes, const int32_t *lengths, double leak,
+                     double scale_floor, const void *num_leak_pi, const void *den_leak_pi,
+                     void *workspace, size_t workspace_bytes, void *grad, double *num_log_probs,
+                     double *den_log_probs, int32_t *num_fail, int32_t *den_fail,
+                     double *totals, void *stream);
+
+/*
+ * Parity/debug seam mirroring the numba kernels argument-for-argument (f64,
+ * caller-allocated outputs written in place, trellis layouts (B,T+1,S_max)).
+ * `expl` is the shifted emission probability array (B,T,D) f64.
+ */
+int lfmmi_forward_kernel(const lfmmi_graphs *graphs, const int64_t *row_map, int32_t batch,
+                         int32_t max_frames, int32_t num_pdfs, const double *expl,
+                         const int32_t *lengths, double leak, const double *leak_pi,
+                         double scale_floor, double *alpha, double *scales,
+                         int64_t *fail_frames, void *stream);
+
+int lfmmi_backward_kernel(const lfmmi_graphs *graphs, const int64_t *row_map, int32_t batch,
+                          int32_t max_frames, int32_t num_pdfs, const double *expl,
+                          const int32_t *lengths, const double *scales, double leak,
+                          const double *leak_pi, const int64_t *fail_frames, double *beta,
+                          void *stream);
+
+int lfmmi_posterior_kernel(const lfmmi_graphs *graphs, const int64_t *row_map, int32_t batch,
+                           int32_t max_frames, int32_t num_pdfs, const double *expl,
+                           const int32_t *lengths, const double *alpha, const double *beta,
+                           const int64_t *fail_frames, double *gamma, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFMMI_H_ */

@@ -1,0 +1,297 @@
+// Host-side graph ingestion: reference padded ChainGraphBatch arrays ->
+// device-resident packed CSR layouts (one cudaMalloc per graph batch).
+//
+// Replaces ChainGraphBatch._build (/root/reference/pkg/src/chainloss/graph.py:236-301)
+// plus the device upload the reference never needed.  Three arc orders are
+// materialised per graph row:
+//   in_*  : CSR by destination state — the reference's backward_* order
+//           (graph.py:150-154), consumed by the forward recursion;
+//   out_* : CSR by source state — the reference's forward_* order
+//           (graph.py:144-148), consumed by the backward recursion;
+//   pa_*  : arcs grouped by pdf id and cut into chunks of <= chunk_len arcs,
+//           consumed by the fused posterior gather (replaces the reference's
+//           scatter over all arcs, _kernels.py:211-224, by a deterministic
+//           per-pdf gather).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "lfmmi_internal.h"
+
+namespace lfmmi {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int check_cuda(cudaError_t err, const char *what) {
+  if (err == cudaSuccess) return LFMMI_OK;
+  return set_error(LFMMI_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(err));
+}
+
+}  // namespace lfmmi
+
+using namespace lfmmi;
+
+extern "C" const char *lfmmi_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char *lfmmi_version(void) { return "paper_2005_09824_b200 lfmmi 0.1.0 (sm_100a)"; }
+
+namespace {
+
+struct HostPack {
+  std::vector<int> desc;
+  std::vector<int> in_ptr, in_src, in_pdf;
+  std::vector<float> in_p32;
+  std::vector<double> in_p64;
+  std::vector<int> out_ptr, out_dst, out_pdf;
+  std::vector<float> out_p32;
+  std::vector<double> out_p64;
+  std::vector<int> pa_src, pa_dst;
+  std::vector<float> pa_p32;
+  std::vector<double> pa_p64;
+  std::vector<int> chunk_begin, chunk_end, chunk_pdf, pdf_chunk_ptr;
+  std::vector<float> fin32;
+  std::vector<double> fin64;
+};
+
+// Chunk length for the pdf-grouped posterior gather: aim for about one chunk
+// per thread of the largest block (1024), never longer than needed.
+int chunk_len_for(int num_arcs) { return std::max(2, (num_arcs + 1023) / 1024); }
+
+template <typename T>
+size_t align_up(size_t x) {
+  (void)sizeof(T);
+  return (x + 255) & ~size_t(255);
+}
+
+}  // namespace
+
+extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t max_arcs,
+                                   int32_t num_pdfs, const int64_t *row_num_states,
+                                   const int64_t *row_num_arcs, const uint32_t *fw_from,
+                                   const uint32_t *fw_to, const uint32_t *fw_pdf,
+                                   const double *fw_prob, const uint32_t *bw_from,
+                                   const uint32_t *bw_to, const uint32_t *bw_pdf,
+                                   const double *bw_prob, const double *final_probs,
+                                   const uint32_t *initial_states, lfmmi_graphs **out) {
+  if (!out) return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create: out is NULL");
+  *out = nullptr;
+  if (num_rows < 1 || max_states < 1 || max_arcs < 0 || num_pdfs < 1)
+    return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create: bad sizes");
+  if (!row_num_states || !row_num_arcs || !fw_from || !fw_to || !fw_pdf || !fw_prob ||
+      !final_probs || !initial_states)
+    return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create: NULL input array");
+  const bool have_bw = bw_from && bw_to && bw_pdf && bw_prob;
+
+  HostPack h;
+  h.desc.resize(size_t(num_rows) * kDescInts, 0);
+  int max_chunks = 0, max_in = 0, max_out = 0;
+  for (int r = 0; r < num_rows; ++r) {
+    const int S = int(row_num_states[r]);
+    const int I = int(row_num_arcs[r]);
+    if (S < 1 || S > max_states || I < 0 || I > max_arcs)
+      return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create: row " + std::to_string(r) +
+                                              " has out-of-range state/arc count");
+    const size_t base = size_t(r) * size_t(max_arcs);
+    for (int i = 0; i < I; ++i) {
+      if (fw_from[base + i] >= uint32_t(S) || fw_to[base + i] >= uint32_t(S) ||
+          fw_pdf[base + i] >= uint32_t(num_pdfs))
+        return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create: row " + std::to_string(r) +
+                                                " arc " + std::to_string(i) + " out of range");
+    }
+    if (initial_states[r] >= uint32_t(S))
+      return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create: initial state out of range");
+
+    int *d = &h.desc[size_t(r) * kDescInts];
+    d[kS] = S;
+    d[kI] = I;
+    d[kInit] = int(initial_states[r]);
+    d[kStateOff] = int(h.fin64.size());
+    d[kPtrOff] = int(h.in_ptr.size());
+    d[kArcOff] = int(h.in_src.size());
+    d[kChunkOff] = int(h.chunk_begin.size());
+    d[kPdfPtrOff] = int(h.pdf_chunk_ptr.size());
+
+    for (int s = 0; s < S; ++s) {
+      const double f = final_probs[size_t(r) * max_states + s];
+      h.fin64.push_back(f);
+      h.fin32.push_back(float(f));
+    }
+
+    // out-CSR: the reference forward_* order is already sorted by source.
+    std::vector<int> cnt_out(S + 1, 0), cnt_in(S + 1, 0);
+    for (int i = 0; i < I; ++i) cnt_out[fw_from[base + i] + 1]++;
+    // in-CSR: reference backward_* order when given, else stable sort by destination.
+    std::vector<int> in_order(I);
+    if (have_bw) {
+      for (int i = 0; i < I; ++i) cnt_in[bw_to[base + i] + 1]++;
+    } else {
+      for (int i = 0; i < I; ++i) cnt_in[fw_to[base + i] + 1]++;
+      std::iota(in_order.begin(), in_order.end(), 0);
+      std::stable_sort(in_order.begin(), in_order.end(), [&](int x, int y) {
+        return fw_to[base + x] < fw_to[base + y];
+      });
+    }
+    int mi = 0, mo = 0;
+    for (int s = 0; s < S; ++s) {
+      mi = std::max(mi, cnt_in[s + 1]);
+      mo = std::max(mo, cnt_out[s + 1]);
+    }
+    for (int s = 0; s < S; ++s) {
+      cnt_in[s + 1] += cnt_in[s];
+      cnt_out[s + 1] += cnt_out[s];
+    }
+    d[kMaxInDeg] = mi;
+    d[kMaxOutDeg] = mo;
+    max_in = std::max(max_in, mi);
+    max_out = std::max(max_out, mo);
+    for (int s = 0; s <= S; ++s) {
+      h.in_ptr.push_back(cnt_in[s]);
+      h.out_ptr.push_back(cnt_out[s]);
+    }
+    for (int i = 0; i < I; ++i) {
+      h.out_dst.push_back(int(fw_to[base + i]));
+      h.out_pdf.push_back(int(fw_pdf[base + i]));
+      h.out_p64.push_back(fw_prob[base + i]);
+      h.out_p32.push_back(float(fw_prob[base + i]));
+      if (have_bw) {
+        h.in_src.push_back(int(bw_from[base + i]));
+        h.in_pdf.push_back(int(bw_pdf[base + i]));
+        h.in_p64.push_back(bw_prob[base + i]);
+        h.in_p32.push_back(float(bw_prob[base + i]));
+      } else {
+        const int j = in_order[i];
+        h.in_src.push_back(int(fw_from[base + j]));
+        h.in_pdf.push_back(int(fw_pdf[base + j]));
+        h.in_p64.push_back(fw_prob[base + j]);
+        h.in_p32.push_back(float(fw_prob[base + j]));
+      }
+    }
+
+    // pdf-grouped arcs (stable by the forward_* order) cut into chunks.
+    std::vector<int> pa(I);
+    std::iota(pa.begin(), pa.end(), 0);
+    std::stable_sort(pa.begin(), pa.end(),
+                     [&](int x, int y) { return fw_pdf[base + x] < fw_pdf[base + y]; });
+    for (int i = 0; i < I; ++i) {
+      const int j = pa[i];
+      h.pa_src.push_back(int(fw_from[base + j]));
+      h.pa_dst.push_back(int(fw_to[base + j]));
+      h.pa_p64.push_back(fw_prob[base + j]);
+      h.pa_p32.push_back(float(fw_prob[base + j]));
+    }
+    const int clen = chunk_len_for(I);
+    int nchunks = 0;
+    int i = 0;
+    for (int pdf = 0; pdf < num_pdfs; ++pdf) {
+      h.pdf_chunk_ptr.push_back(nchunks);
+      int j = i;
+      while (j < I && int(fw_pdf[base + pa[j]]) == pdf) ++j;
+      for (int c = i; c < j; c += clen) {
+        h.chunk_begin.push_back(c);
+        h.chunk_end.push_back(std::min(j, c + clen));
+        h.chunk_pdf.push_back(pdf);
+        ++nchunks;
+      }
+      i = j;
+    }
+    h.pdf_chunk_ptr.push_back(nchunks);
+    d[kNumChunks] = nchunks;
+    max_chunks = std::max(max_chunks, nchunks);
+  }
+
+  // One device allocation, 256-byte aligned sub-buffers.
+  struct Piece {
+    const void *src;
+    size_t bytes;
+    const void **dst;
+  };
+  auto *g = new lfmmi_graphs();
+  g->num_rows = num_rows;
+  g->max_states = max_states;
+  g->max_arcs = max_arcs;
+  g->num_pdfs = num_pdfs;
+  g->max_chunks = max_chunks;
+  g->max_in_deg = max_in;
+  g->max_out_deg = max_out;
+  DevGraphs &dv = g->dev;
+  std::vector<Piece> pieces;
+  auto add = [&](const auto &vec, const auto **dst) {
+    using T = typename std::decay_t<decltype(vec)>::value_type;
+    pieces.push_back({vec.data(), vec.size() * sizeof(T), reinterpret_cast<const void **>(dst)});
+  };
+  add(h.desc, &dv.desc);
+  add(h.in_ptr, &dv.in_ptr);
+  add(h.in_src, &dv.in_src);
+  add(h.in_pdf, &dv.in_pdf);
+  add(h.in_p32, &dv.in_p32);
+  add(h.in_p64, &dv.in_p64);
+  add(h.out_ptr, &dv.out_ptr);
+  add(h.out_dst, &dv.out_dst);
+  add(h.out_pdf, &dv.out_pdf);
+  add(h.out_p32, &dv.out_p32);
+  add(h.out_p64, &dv.out_p64);
+  add(h.pa_src, &dv.pa_src);
+  add(h.pa_dst, &dv.pa_dst);
+  add(h.pa_p32, &dv.pa_p32);
+  add(h.pa_p64, &dv.pa_p64);
+  add(h.chunk_begin, &dv.chunk_begin);
+  add(h.chunk_end, &dv.chunk_end);
+  add(h.chunk_pdf, &dv.chunk_pdf);
+  add(h.pdf_chunk_ptr, &dv.pdf_chunk_ptr);
+  add(h.fin32, &dv.fin32);
+  add(h.fin64, &dv.fin64);
+  size_t total = 0;
+  std::vector<size_t> offs;
+  for (auto &p : pieces) {
+    offs.push_back(total);
+    total += align_up<char>(std::max<size_t>(p.bytes, 16));
+  }
+  std::vector<char> staging(total, 0);
+  for (size_t k = 0; k < pieces.size(); ++k)
+    if (pieces[k].bytes) std::memcpy(staging.data() + offs[k], pieces[k].src, pieces[k].bytes);
+  void *dev = nullptr;
+  int rc = check_cuda(cudaMalloc(&dev, total), "cudaMalloc(graph pack)");
+  if (rc) {
+    delete g;
+    return rc;
+  }
+  rc = check_cuda(cudaMemcpy(dev, staging.data(), total, cudaMemcpyHostToDevice),
+                  "cudaMemcpy(graph pack)");
+  if (rc) {
+    cudaFree(dev);
+    delete g;
+    return rc;
+  }
+  for (size_t k = 0; k < pieces.size(); ++k)
+    *pieces[k].dst = static_cast<const char *>(dev) + offs[k];
+  g->device_block = dev;
+  g->device_bytes = total;
+  *out = g;
+  return LFMMI_OK;
+}
+
+extern "C" int lfmmi_graphs_destroy(lfmmi_graphs *graphs) {
+  if (!graphs) return LFMMI_OK;
+  int rc = LFMMI_OK;
+  if (graphs->device_block) rc = check_cuda(cudaFree(graphs->device_block), "cudaFree(graph pack)");
+  delete graphs;
+  return rc;
+}
+
+extern "C" int lfmmi_graphs_info(const lfmmi_graphs *graphs, int32_t *num_rows,
+                                 int32_t *max_states, int32_t *max_arcs, int32_t *num_pdfs) {
+  if (!graphs) return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_info: NULL handle");
+  if (num_rows) *num_rows = graphs->num_rows;
+  if (max_states) *max_states = graphs->max_states;
+  if (max_arcs) *max_arcs = graphs->max_arcs;
+  if (num_pdfs) *num_pdfs = graphs->num_pdfs;
+  return LFMMI_OK;
+}

@@ -1,0 +1,62 @@
+// Internal declarations shared by the graph packer and the kernels.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "lfmmi.h"
+
+namespace lfmmi {
+
+// Per-row descriptor ints (device array desc[num_rows * kDescInts]).
+enum DescField : int {
+  kS = 0,          // number of states
+  kI = 1,          // number of arcs
+  kInit = 2,       // initial state
+  kStateOff = 3,   // offset into per-state arrays (finals)
+  kPtrOff = 4,     // offset into in_ptr / out_ptr (S + 1 entries per row)
+  kArcOff = 5,     // offset into every per-arc array
+  kChunkOff = 6,   // offset into chunk arrays
+  kNumChunks = 7,  // number of pdf chunks in this row
+  kPdfPtrOff = 8,  // offset into pdf_chunk_ptr (D + 1 entries per row)
+  kMaxInDeg = 9,
+  kMaxOutDeg = 10,
+  kDescInts = 12
+};
+
+// Device-side view of a packed graph batch (passed by value to kernels).
+struct DevGraphs {
+  const int *desc;
+  // CSR by destination state (reference "backward_*" layout, graph.py:150-154)
+  const int *in_ptr, *in_src, *in_pdf;
+  const float *in_p32;
+  const double *in_p64;
+  // CSR by source state (reference "forward_*" layout, graph.py:144-148)
+  const int *out_ptr, *out_dst, *out_pdf;
+  const float *out_p32;
+  const double *out_p64;
+  // arcs grouped by pdf, cut into chunks (new: deterministic posterior gather)
+  const int *pa_src, *pa_dst;
+  const float *pa_p32;
+  const double *pa_p64;
+  const int *chunk_begin, *chunk_end, *chunk_pdf, *pdf_chunk_ptr;
+  const float *fin32;
+  const double *fin64;
+};
+
+}  // namespace lfmmi
+
+struct lfmmi_graphs {
+  int32_t num_rows = 0, max_states = 0, max_arcs = 0, num_pdfs = 0;
+  int32_t max_chunks = 0, max_in_deg = 0, max_out_deg = 0;
+  void *device_block = nullptr;
+  size_t device_bytes = 0;
+  lfmmi::DevGraphs dev{};
+};
+
+namespace lfmmi {
+int set_error(int code, const std::string &msg);
+int check_cuda(cudaError_t err, const char *what);
+}  // namespace lfmmi

@@ -1,0 +1,203 @@
+"""LF-MMI objective: drop-in ``chain_loss`` plus the paper's torch API.
+
+* :func:`chain_loss` — same signature, result type and failure semantics as
+  /root/reference/pkg/src/chainloss/loss.py:42-84 (numpy in, numpy out,
+  sorted batch order, ``RuntimeError`` when every utterance fails).  One C-ABI
+  call (``lfmmi_chain_loss``): numerator launch writes gamma_num into the
+  gradient, denominator launch subtracts gamma_den in place, a tiny
+  reduction produces {objective, frames, failed} on device.
+* :func:`chain_loss_device` — the same on CUDA tensors, no host sync.
+* :class:`ChainFunction` / :class:`ChainLoss` — the paper's
+  ``autograd.Function`` / ``nn.Module``.  With a process group
+  the three scalar totals are all-reduced (NCCL over NVLink) so the
+  normalised loss equals the single-GPU one; gradients are never exchanged.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _backend
+from .forward_backward import (FBOptions, _check_compatible, _dtype, _leak_distribution,
+                               _to_device, _workspace)
+from .graph import ChainGraphBatch, device_graphs
+
+__all__ = ["ChainLossResult", "chain_loss", "chain_loss_device", "ChainFunction", "ChainLoss"]
+
+
+@dataclass
+class ChainLossResult:
+    """Objective, loss and gradient of one batch, in sorted batch order (loss.py:22-39)."""
+
+    objective: float
+    loss: float
+    grad: np.ndarray
+    per_utt: list
+    num_failed: int
+
+
+def chain_loss_device(values, lengths, numerators, denominator, opts: FBOptions = FBOptions(), *,
+                      total_frames=None, grad=None):
+    """LF-MMI on device tensors.
+
+    ``values`` (B, T, D) CUDA float32/float64; ``lengths`` (B,) CUDA int32.
+    Returns ``(grad, num_logp, den_logp, num_fail, den_fail, totals)`` where
+    ``grad = gamma_num - gamma_den`` (zero rows for failed / padded frames)
+    and ``totals = [sum_ok(num - den), sum_ok T_b, #failed]`` (f64).
+    """
+    import torch
+
+    ext = _backend.require_cuda()
+    dev = values.device
+    B, T, D = values.shape
+    ng = device_graphs(numerators, dev)
+    dgr = device_graphs(denominator, dev)
+    pn = _leak_distribution(numerators, opts)
+    pd = _leak_distribution(denominator, opts)
+    pn = None if pn is None else torch.as_tensor(pn, dtype=values.dtype, device=dev)
+    pd = None if pd is None else torch.as_tensor(pd, dtype=values.dtype, device=dev)
+    if total_frames is None:
+        total_frames = B * T
+    prec = 1 if values.dtype == torch.float64 else 0
+    ws = _workspace(dev, ext.workspace_size(max(ng.max_states, dgr.max_states),
+                                            int(total_frames), prec))
+    if grad is None:
+        grad = torch.empty_like(values)
+    f64 = dict(dtype=torch.float64, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    num_lp, den_lp = torch.empty(B, **f64), torch.empty(B, **f64)
+    num_fail, den_fail = torch.empty(B, **i32), torch.empty(B, **i32)
+    totals = torch.empty(3, **f64)
+    ext.chain_loss(ng.handle, ng.row_map, dgr.handle, dgr.row_map, values, lengths,
+                   float(opts.leak_coefficient), float(opts.scale_floor), pn, pd, ws, grad,
+                   num_lp, den_lp, num_fail, den_fail, totals)
+    return grad, num_lp, den_lp, num_fail, den_fail, totals
+
+
+def chain_loss(batch, numerators, denominator, opts: FBOptions = FBOptions(),
+               normalize_by_frames: bool = True, precision: str | None = None) -> ChainLossResult:
+    """MMI objective and gradient for one batch (loss.py:42-84), computed on the GPU."""
+    _check_compatible(batch, numerators)
+    _check_compatible(batch, denominator)
+    _backend.require_cuda()
+    dev, values, lengths = _to_device(batch, _dtype(precision))
+    grad, num_lp, den_lp, num_fail, den_fail, totals = chain_loss_device(
+        values, lengths, numerators, denominator, opts, total_frames=batch.total_frames)
+    tot = totals.cpu().numpy()
+    num_failed = int(round(tot[2]))
+    if num_failed == batch.batch_size:
+        raise RuntimeError(f"all {batch.batch_size} utterances failed numerically")
+    objective = float(tot[0])
+    frames = int(round(tot[1]))
+    loss = -objective / frames if normalize_by_frames else -objective
+    nl, dl = num_lp.cpu().numpy(), den_lp.cpu().numpy()
+    per_utt = [(float(nl[b]), float(dl[b])) for b in range(batch.batch_size)]
+    import torch
+
+    return ChainLossResult(objective=objective, loss=loss,
+                           grad=grad.to(torch.float64).cpu().numpy(), per_utt=per_utt,
+                           num_failed=num_failed)
+
+
+# ------------------------------------------------------------------- torch API
+def _as_graph_batch(graphs, batch_size):
+    if isinstance(graphs, (list, tuple)):
+        return ChainGraphBatch.from_graphs(graphs)
+    if hasattr(graphs, "forward_from") and not hasattr(graphs, "row_map"):  # a single ChainGraph
+        return ChainGraphBatch.broadcast(graphs, batch_size)
+    return graphs
+
+
+def _autograd_function():
+    import torch
+
+    class _ChainFunction(torch.autograd.Function):
+        """LF-MMI loss as an autograd function (paper's ``ChainFunction``).
+
+        ``apply(input, input_lengths, numerators, denominator, opts,
+        normalize_by_frames, process_group)`` -> scalar loss
+        ``-sum_ok(logP_num - logP_den) / frames`` (or un-normalised).
+        ``input`` is (B, T, D) on CUDA in any length order; ``numerators`` is
+        aligned with it.  Backward returns ``-(gamma_num - gamma_den) / frames``
+        scaled by the incoming gradient.
+        """
+
+        @staticmethod
+        def forward(ctx, input, input_lengths, numerators, denominator, opts=FBOptions(),
+                    normalize_by_frames=True, process_group=None):
+            if not input.is_cuda:
+                raise _backend.BackendUnavailable("ChainFunction needs a CUDA input tensor")
+            x = input.detach().contiguous()
+            if x.dtype not in (torch.float32, torch.float64):
+                x = x.float()
+            lengths = input_lengths.to(device=x.device, dtype=torch.int32).contiguous()
+            B = x.shape[0]
+            nums = _as_graph_batch(numerators, B)
+            den = _as_graph_batch(denominator, B)
+            grad, _, _, _, _, totals = chain_loss_device(x, lengths, nums, den, opts)
+            if process_group is not None:
+                import torch.distributed as dist
+
+                dist.all_reduce(totals, op=dist.ReduceOp.SUM, group=process_group)
+            scale = (1.0 / totals[1]) if normalize_by_frames else totals.new_ones(())
+            loss = -totals[0] * scale
+            ctx.save_for_backward(grad, scale)
+            ctx.in_dtype = input.dtype
+            return loss.to(input.dtype)
+
+        @staticmethod
+        def backward(ctx, grad_output):
+            grad, scale = ctx.saved_tensors
+            g = grad * (-(grad_output.to(torch.float64) * scale)).to(grad.dtype)
+            return g.to(ctx.in_dtype), None, None, None, None, None, None
+
+    return _ChainFunction
+
+
+class _LazyFunction:
+    _fn = None
+
+    def __getattr__(self, name):
+        if _LazyFunction._fn is None:
+            _LazyFunction._fn = _autograd_function()
+        return getattr(_LazyFunction._fn, name)
+
+
+ChainFunction = _LazyFunction()
+
+
+def _module_base():
+    import torch
+
+    return torch.nn.Module
+
+
+class ChainLoss(_module_base()):
+    """``nn.Module`` wrapper (paper's ``ChainLoss``): holds the denominator graph.
+
+    ``ChainLoss(den_graph, opts=FBOptions(), normalize_by_frames=True,
+    process_group=None)(input, input_lengths, num_graphs)`` -> scalar loss.
+    """
+
+    def __init__(self, den_graph, opts: FBOptions = FBOptions(), normalize_by_frames: bool = True,
+                 process_group=None):
+        super().__init__()
+        self.den_graph = den_graph
+        self.opts = opts
+        self.normalize_by_frames = normalize_by_frames
+        self.process_group = process_group
+        self._den_cache = {}
+
+    def _den_batch(self, batch_size):
+        if hasattr(self.den_graph, "row_map"):
+            return self.den_graph
+        if batch_size not in self._den_cache:
+            self._den_cache[batch_size] = ChainGraphBatch.broadcast(self.den_graph, batch_size)
+        return self._den_cache[batch_size]
+
+    def forward(self, input, input_lengths, num_graphs):
+        den = self._den_batch(input.shape[0])
+        return ChainFunction.apply(input, input_lengths, num_graphs, den, self.opts,
+                                   self.normalize_by_frames, self.process_group)

@@ -1,0 +1,250 @@
+"""GPU parity: CUDA path (through the C-ABI) vs the pinned oracle / golden vectors.
+
+Tolerances (BASELINE.json north_star): fp32 production path — objective
+within 1e-5 relative, gradient within 1e-4 absolute.  fp64 fused path —
+1e-10.  f64 parity kernels (three-phase seam) — bit-exact, since they follow
+the reference operation order with no FMA contraction.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2005_09824_b200 as P
+from golden_util import load, names
+from oracle import oracle as O
+from paper_2005_09824_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+FP32_OBJ_REL = 1e-5
+FP32_GRAD_ABS = 1e-4
+FP64_TOL = 1e-10
+
+
+def _rel(a, b):
+    return abs(a - b) / max(1.0, abs(b))
+
+
+# ------------------------------------------------------------ golden vectors
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("name", names())
+def test_chain_loss_vs_golden(cuda, name, precision):
+    batch, nums, den, leak, z = load(name)
+    opts = P.FBOptions(leak_coefficient=leak)
+    if int(z["all_failed"]):
+        with pytest.raises(RuntimeError, match="failed"):
+            P.chain_loss(batch, nums, den, opts, precision=precision)
+        return
+    res = P.chain_loss(batch, nums, den, opts, precision=precision)
+    otol, gtol = (FP32_OBJ_REL, FP32_GRAD_ABS) if precision == "fp32" else (FP64_TOL, FP64_TOL)
+    assert _rel(res.objective, float(z["objective"])) <= otol
+    assert np.abs(res.grad - z["grad"]).max() <= gtol
+    assert res.num_failed == int(z["num_failed"])
+    pu = np.array(res.per_utt)
+    np.testing.assert_array_equal(np.isnan(pu), np.isnan(z["per_utt"]))
+    ok = ~np.isnan(z["per_utt"])
+    assert np.all(np.abs(pu[ok] - z["per_utt"][ok]) <= otol * np.maximum(1, np.abs(z["per_utt"][ok])))
+    # normalisation (loss.py:71-72)
+    assert _rel(res.loss, float(z["loss"])) <= otol
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("name", names())
+def test_forward_backward_vs_golden(cuda, name, precision):
+    batch, nums, den, leak, z = load(name)
+    opts = P.FBOptions(leak_coefficient=leak)
+    tol = 1e-5 if precision == "fp32" else FP64_TOL
+    for side, g in (("num", nums), ("den", den)):
+        fb = P.forward_backward(batch, g, opts, precision=precision)
+        np.testing.assert_array_equal(fb.failure_frames, z[f"{side}_failure_frames"])
+        ref = z[f"{side}_log_probs"]
+        np.testing.assert_array_equal(np.isnan(fb.log_probs), np.isnan(ref))
+        ok = ~np.isnan(ref)
+        assert np.all(np.abs(fb.log_probs[ok] - ref[ok]) <= tol * np.maximum(1, np.abs(ref[ok])))
+        assert np.abs(fb.posteriors - z[f"{side}_posteriors"]).max() <= (
+            FP32_GRAD_ABS if precision == "fp32" else FP64_TOL)
+        np.testing.assert_allclose(fb.scale_logs, z[f"{side}_scale_logs"], rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("name", [n for n in names() if not n.startswith("toy")])
+def test_parity_kernels_bit_exact(cuda, name):
+    """lfmmi_{forward,backward,posterior}_kernel == reference numba kernels, bitwise."""
+    import torch
+
+    from paper_2005_09824_b200 import _backend
+
+    ext = _backend.ext()
+    batch, nums, den, leak, z = load(name)
+    expl, _ = O.emissions(batch.values, batch.lengths)  # reference host glue (numpy)
+    dev = torch.device("cuda", 0)
+    for side, g in (("num", nums), ("den", den)):
+        dg = P.device_graphs(g, dev)
+        pi = O.leak_distribution(g)
+        B, T, D = batch.values.shape
+        S = g.max_states
+        a = torch.zeros((B, T + 1, S), dtype=torch.float64, device=dev)
+        sc = torch.ones((B, T), dtype=torch.float64, device=dev)
+        fl = torch.full((B,), -1, dtype=torch.int64, device=dev)
+        ex = torch.tensor(expl, device=dev)
+        ln = torch.tensor(batch.lengths, dtype=torch.int32, device=dev)
+        pit = torch.tensor(pi, device=dev)
+        ext.forward_kernel(dg.handle, dg.row_map, ex, ln, leak, pit, 1e-300, a, sc, fl)
+        np.testing.assert_array_equal(a.cpu().numpy(), z[f"{side}_alpha"])
+        np.testing.assert_array_equal(fl.cpu().numpy(), z[f"{side}_failure_frames"])
+        be = torch.zeros_like(a)
+        ext.backward_kernel(dg.handle, dg.row_map, ex, ln, sc, leak, pit, fl, be)
+        np.testing.assert_array_equal(be.cpu().numpy(), z[f"{side}_beta"])
+        gm = torch.zeros((B, T, D), dtype=torch.float64, device=dev)
+        ext.posterior_kernel(dg.handle, dg.row_map, ex, ln, a, be, fl, gm)
+        np.testing.assert_array_equal(gm.cpu().numpy(), z[f"{side}_posteriors"])
+
+
+@pytest.mark.parametrize("name", ["ka_two_state", "rand00", "rand01", "rand02"])
+def test_three_phase_api(cuda, name):
+    batch, nums, den, leak, z = load(name)
+    opts = P.FBOptions(leak_coefficient=leak)
+    fb = P.forward_backward(batch, den, opts, keep_trellis=True)
+    np.testing.assert_allclose(fb.alpha, z["den_alpha"], rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(fb.beta, z["den_beta"], rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(fb.posteriors, z["den_posteriors"], atol=1e-12)
+    fwd = P.forward(batch, den, opts)
+    beta = P.backward(batch, den, opts, fwd)
+    gamma = P.occupation_posteriors(batch, den, fwd, beta)
+    np.testing.assert_array_equal(gamma, fb.posteriors)
+
+
+# ------------------------------------------------- BASELINE configs vs oracle
+@pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
+                                               ("wsj_biphone", 4), ("sweep", 6)])
+def test_configs_vs_oracle(cuda, config, batch_size):
+    w = synth.make_workload(config, seed=3, batch_size=batch_size)
+    batch, nums, den = w.build(P)
+    res = P.chain_loss(batch, nums, den)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    assert _rel(res.objective, ref.objective) <= FP32_OBJ_REL
+    assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
+    assert res.num_failed == ref.num_failed == 0
+
+
+# ------------------------------------------ size-independent properties (full C2)
+@pytest.fixture(scope="module")
+def c2():
+    w = synth.make_workload("wsj_mono", seed=0)
+    return w.build(P)
+
+
+def test_c2_grad_structure(cuda, c2):
+    batch, nums, den = c2
+    res = P.chain_loss(batch, nums, den)
+    for b in range(batch.batch_size):
+        n = int(batch.lengths[b])
+        assert np.abs(res.grad[b, :n].sum(axis=1)).max() <= 1e-4   # rows sum to 0
+        assert np.all(res.grad[b, n:] == 0.0)                        # padding is zero
+    # posteriors are distributions
+    fb = P.forward_backward(batch, den)
+    rs = np.concatenate([fb.posteriors[b, : batch.lengths[b]].sum(axis=1)
+                         for b in range(batch.batch_size)])
+    assert np.abs(rs - 1.0).max() <= 1e-4
+
+
+def test_c2_deterministic_and_batch_independent(cuda, c2):
+    batch, nums, den = c2
+    r1 = P.chain_loss(batch, nums, den)
+    r2 = P.chain_loss(batch, nums, den)
+    assert r1.objective == r2.objective and np.array_equal(r1.grad, r2.grad)
+    for b in (0, 77, batch.batch_size - 1):
+        n = int(batch.lengths[b])
+        solo = P.make_batch([batch.values[b, :n]])
+        rs = P.chain_loss(solo, P.ChainGraphBatch.from_graphs([nums.graph(b)]),
+                          P.ChainGraphBatch.broadcast(den.graph(0), 1))
+        assert rs.per_utt[0] == r1.per_utt[b]
+        assert np.array_equal(rs.grad[0], r1.grad[b, :n])
+
+
+def test_c2_nan_poisoned_padding(cuda, c2):
+    batch, nums, den = c2
+    clean = P.chain_loss(batch, nums, den)
+    v = batch.values.copy()
+    for b in range(batch.batch_size):
+        v[b, int(batch.lengths[b]):] = np.nan
+    dirty = P.chain_loss(P.LogLikBatch(v, batch.lengths, batch.valid_batch_sizes,
+                                       batch.order_map), nums, den)
+    assert clean.objective == dirty.objective
+    assert np.array_equal(clean.grad, dirty.grad)
+
+
+def test_c2_shift_equivariance(cuda, c2):
+    batch, nums, den = c2
+    base = P.forward_backward(batch, den)
+    v = batch.values.copy()
+    v[:, 10, :] += 0.75
+    shifted = P.forward_backward(P.LogLikBatch(v, batch.lengths, batch.valid_batch_sizes,
+                                               batch.order_map), den)
+    np.testing.assert_allclose(shifted.log_probs, base.log_probs + 0.75, rtol=1e-6)
+    assert np.abs(shifted.posteriors[:, 10] - base.posteriors[:, 10]).max() <= 1e-5
+
+
+# ------------------------------------------------------------- edge cases
+def test_failure_semantics(cuda):
+    batch, nums, den, leak, z = load("ka_failure")
+    res = P.chain_loss(batch, nums, den, P.FBOptions(leak_coefficient=0.0))
+    assert res.num_failed == 1
+    assert np.all(res.grad[1] == 0.0)
+    num_lp, den_lp = res.per_utt[1]
+    assert math.isnan(num_lp) and not math.isnan(den_lp)
+
+
+def test_custom_leak_distribution(cuda):
+    w = synth.make_workload("toy", seed=5)
+    batch, nums, den = w.build(P)
+    rng = np.random.default_rng(1)
+    pi = rng.random(den.max_states)
+    pi /= pi.sum()
+    res = P.chain_loss(batch, P.ChainGraphBatch.from_graphs([den.graph(0)] * batch.batch_size),
+                       den, P.FBOptions(leak_coefficient=1e-2, leak_distribution=pi),
+                       precision="fp64")
+    assert abs(res.objective) <= 1e-9 and np.abs(res.grad).max() <= 1e-9
+    fb = P.forward_backward(batch, den, P.FBOptions(leak_coefficient=1e-2, leak_distribution=pi),
+                            precision="fp64")
+    ref = O.forward_backward(batch, den, leak=1e-2, leak_dist=pi)
+    np.testing.assert_allclose(fb.log_probs, ref.log_probs, rtol=1e-10)
+    np.testing.assert_allclose(fb.posteriors, ref.posteriors, atol=1e-10)
+
+
+def test_single_frame_and_ragged(cuda):
+    rng = np.random.default_rng(3)
+    loop = P.ChainGraph([(0, 0, 0, 0.5), (0, 0, 1, 0.5)], 1, 2, 0, [1.0])
+    seqs = [rng.normal(size=(t, 2)) for t in (1, 7, 1, 3)]
+    batch = P.make_batch(seqs)
+    nums = P.ChainGraphBatch.from_graphs([loop] * 4)
+    den = P.ChainGraphBatch.broadcast(loop, 4)
+    res = P.chain_loss(batch, nums, den, precision="fp64")
+    ref = O.chain_loss(batch, nums, den)
+    assert abs(res.objective - ref.objective) <= 1e-12
+    np.testing.assert_allclose(res.grad, ref.grad, atol=1e-12)
+
+
+def test_chain_function_autograd(cuda):
+    import torch
+
+    w = synth.make_workload("toy", seed=2)
+    batch, nums, den = w.build(P)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    x = torch.tensor(batch.values, dtype=torch.float32, device="cuda", requires_grad=True)
+    loss = P.ChainFunction.apply(x, torch.tensor(batch.lengths), nums, den)
+    (2.0 * loss).backward()
+    frames = int(batch.lengths.sum())
+    assert _rel(float(loss), ref.loss) <= 1e-5
+    assert np.abs(x.grad.double().cpu().numpy() + 2.0 * ref.grad / frames).max() <= 1e-5
+    mod = P.ChainLoss(den.graph(0))
+    l2 = mod(x, torch.tensor(batch.lengths), nums)
+    assert float(l2) == float(loss)
+
+
+def test_pdf_mismatch_raises(cuda):
+    loop = P.ChainGraph([(0, 0, 0, 1.0)], 1, 1, 0, [1.0])
+    batch = P.make_batch([np.zeros((2, 2))])
+    with pytest.raises(ValueError, match="pdf dimension"):
+        P.chain_loss(batch, P.ChainGraphBatch.broadcast(loop, 1), P.ChainGraphBatch.broadcast(loop, 1))
