@@ -282,11 +282,11 @@ def run_ours(args):
 
     # ---- dominant kernel (denominator pass) timed alone, same inputs -----
     def den_launch():
-        P.forward_backward_device(values, lengths, den, opts, posteriors=grad, mode=1,
+        P.forward_backward_device(values, lengths, den, opts, posteriors=grad, mode=3,
                                   total_frames=frames_local)
 
     def num_launch():
-        P.forward_backward_device(values, lengths, nums, opts, posteriors=grad, mode=0,
+        P.forward_backward_device(values, lengths, nums, opts, posteriors=grad, mode=2,
                                   total_frames=frames_local)
 
     kt = {}
@@ -374,7 +374,7 @@ def run_ours(args):
                        "parallelism": f"dp{world} (sequence-sharded, scalar all-reduce)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "fb_fused_kernel<float,1024> (denominator pass)",
+                         "kernel": "fb_tile_kernel<float,1024> (denominator pass)",
                          "algorithmic_bytes_per_launch": A, "launch_ms": kt["den"],
                          "peak_source": peak_src},
             "kernel_ms": {"den_fused": kt["den"], "num_fused": kt["num"],

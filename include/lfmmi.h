@@ -38,7 +38,9 @@ extern "C" {
 #define LFMMI_F64 1
 
 #define LFMMI_POST_WRITE 0    /* posteriors[b,t,:]  = gamma                     */
-#define LFMMI_POST_SUBTRACT 1 /* posteriors[b,t,:] -= gamma  (grad = num - den) */
+#define LFMMI_POST_SUBTRACT 1 /* posteriors[b,t,:] -= gamma                     */
+#define LFMMI_POST_ADD 2      /* posteriors[b,t,:] += gamma  (grad = num - den) */
+#define LFMMI_POST_NEGATE 3   /* posteriors[b,t,:]  = -gamma                    */
 
 typedef struct lfmmi_graphs lfmmi_graphs;
 
@@ -85,10 +87,11 @@ size_t lfmmi_workspace_size(int32_t max_states, int64_t total_frames, int32_t pr
  *   lengths      (B)        int32  valid frames per item (>= 1)    [device]
  *   leak_pi      (G,S_max)  f32/f64 custom leak distribution, or NULL for uniform 1/S_g
  *   workspace    device scratch of >= lfmmi_workspace_size(...) bytes
- *   posteriors   (B,T,D)    f32/f64  written per `post_mode`; padded rows and failed
- *                           items are zeroed (WRITE) / set to zero (SUBTRACT)
+ *   posteriors   (B,T,D)    f32/f64  written per `post_mode`; rows of failed items
+ *                           are set to zero in every mode; padded rows are zeroed
+ *                           by the writing modes (WRITE, NEGATE)
  *   other_fail   (B) int32 or NULL: items whose other-graph recursion failed get
- *                zero rows (used for the denominator pass of chain_loss)
+ *                zero rows (used for the second pass of chain_loss)
  *   log_probs    (B) f64 out (NaN when failed); fail_frames (B) int32 out (-1 or frame)
  *   scale_logs   (B,T) f64 out or NULL
  * precision selects f32 (LFMMI_F32) or f64 (LFMMI_F64) for all real arrays.
@@ -102,8 +105,8 @@ int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t *row_map, i
                            double *scale_logs, void *stream);
 
 /*
- * LF-MMI objective and gradient for one batch (loss.py:42-84): numerator pass
- * (WRITE) then denominator pass (SUBTRACT) into `grad`, then a reduction of
+ * LF-MMI objective and gradient for one batch (loss.py:42-84): denominator pass
+ * (NEGATE) then numerator pass (ADD) into `grad`, then a reduction of
  * totals[0] = sum_ok(num_lp - den_lp), totals[1] = sum_ok(T_b),
  * totals[2] = #failed   (device f64[3]; sum-reducible across ranks).
  */

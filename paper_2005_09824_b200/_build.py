@@ -26,7 +26,7 @@ TORCH_SO = os.path.join(LIB_DIR, "_lfmmi_torch" + (sysconfig.get_config_var("EXT
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CORE_SOURCES = ["lfmmi_fb.cu", "lfmmi_graph.cpp"]
+CORE_SOURCES = ["lfmmi_api.cu", "lfmmi_group.cu", "lfmmi_tile.cu", "lfmmi_graph.cpp"]
 
 
 def _run(cmd, verbose):
@@ -44,7 +44,8 @@ def _stale(target, sources):
 
 def build_core(verbose=True, force=False):
     srcs = [os.path.join(CSRC, s) for s in CORE_SOURCES]
-    deps = srcs + [os.path.join(CSRC, "lfmmi_internal.h"), os.path.join(INCLUDE, "lfmmi.h")]
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    deps.append(os.path.join(INCLUDE, "lfmmi.h"))
     if not force and not _stale(CORE_SO, deps):
         return CORE_SO
     os.makedirs(LIB_DIR, exist_ok=True)

@@ -1,0 +1,385 @@
+// C-ABI entry points (include/lfmmi.h) + the f64 parity kernels.
+//
+// Dispatch of the fused forward-backward:
+//   * graphs that fit the on-chip tile pack (the denominator) -> fb_tile_kernel
+//     (one 1024-thread CTA per utterance, arc layout resident in shared memory);
+//   * small graphs (numerators) -> fb_group_kernel with a warp-sized group;
+//   * anything else -> fb_group_kernel with a CTA-sized group (arcs via L1/L2).
+// chain_loss = denominator pass (grad = -gamma_den) + numerator pass
+// (grad += gamma_num, zero rows if either side failed) + totals reduction.
+//
+// Parity path (f64): lfmmi_{forward,backward,posterior}_kernel mirror the
+// numba kernels argument-for-argument with the reference's exact operation
+// order (no FMA contraction) for bit-level parity with the reference tests.
+#include <algorithm>
+#include <string>
+#include <type_traits>
+
+#include "lfmmi_device.cuh"
+#include "lfmmi_kernels.h"
+
+namespace lfmmi {
+
+// ---- f64 parity kernels (exact reference operation order) -----------------
+// _kernels.py:54-122.  One CTA per item; per-state sums in CSR order, column
+// sums sequential in state order, no FMA contraction.
+__global__ void fwd_parity_kernel(DevGraphs g, const int64_t *row_map, int B, int T_max, int D,
+                                  int S_max, const double *expl, const int *lengths, double leak,
+                                  const double *leak_pi, double floor, double *alpha,
+                                  double *scales, int64_t *fail) {
+  const int b = blockIdx.x;
+  const int row = int(row_map[b]);
+  const int *desc = g.desc + row * kDescInts;
+  const int S = desc[kS];
+  const int *ptr = g.in_ptr + desc[kPtrOff];
+  const int *src = g.in_src + desc[kArcOff];
+  const int *pdf = g.in_pdf + desc[kArcOff];
+  const double *p = g.in_p64 + desc[kArcOff];
+  const double *fin = g.fin64 + desc[kStateOff];
+  const double *pi = leak_pi + size_t(row) * S_max;
+  const int T = lengths[b];
+  const size_t T1 = size_t(T_max) + 1;
+  __shared__ double s_total;
+  __shared__ int s_fail;
+  double *al = alpha + size_t(b) * T1 * S_max;
+  if (threadIdx.x == 0) {
+    al[desc[kInit]] = 1.0;
+    s_fail = -1;
+  }
+  __syncthreads();
+  for (int t = 1; t <= T; ++t) {
+    const double *prev = al + size_t(t - 1) * S_max;
+    double *col = al + size_t(t) * S_max;
+    const double *e = expl + (size_t(b) * T_max + (t - 1)) * D;
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+      double acc = 0.0;
+      for (int i = ptr[s]; i < ptr[s + 1]; ++i)
+        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(p[i], prev[src[i]]), e[pdf[i]]));
+      if (t == T) acc = __dmul_rn(acc, fin[s]);
+      col[s] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double total = 0.0;
+      for (int s = 0; s < S_max; ++s) total = __dadd_rn(total, col[s]);
+      s_total = total;
+    }
+    __syncthreads();
+    double total = s_total;
+    if (leak > 0.0 && total > 0.0) {
+      for (int s = threadIdx.x; s < S_max; s += blockDim.x)
+        col[s] = __dadd_rn(col[s], __dmul_rn(__dmul_rn(leak, pi[s]), total));
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t2 = 0.0;
+        for (int s = 0; s < S_max; ++s) t2 = __dadd_rn(t2, col[s]);
+        s_total = t2;
+      }
+      __syncthreads();
+      total = s_total;
+    }
+    if (!(total >= floor) || total == INFINITY) {
+      for (int s = threadIdx.x; s < S_max; s += blockDim.x) col[s] = 0.0;
+      if (threadIdx.x == 0) s_fail = t - 1;
+      __syncthreads();
+      break;
+    }
+    const double inv = 1.0 / total;
+    for (int s = threadIdx.x; s < S_max; s += blockDim.x) col[s] = __dmul_rn(col[s], inv);
+    if (threadIdx.x == 0) scales[size_t(b) * T_max + t - 1] = total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) fail[b] = s_fail;
+}
+
+// _kernels.py:125-191.
+__global__ void bwd_parity_kernel(DevGraphs g, const int64_t *row_map, int B, int T_max, int D,
+                                  int S_max, const double *expl, const int *lengths,
+                                  const double *scales, double leak, const double *leak_pi,
+                                  const int64_t *fail, double *beta) {
+  const int b = blockIdx.x;
+  if (fail[b] >= 0) return;
+  const int row = int(row_map[b]);
+  const int *desc = g.desc + row * kDescInts;
+  const int S = desc[kS];
+  const int *ptr = g.out_ptr + desc[kPtrOff];
+  const int *dst = g.out_dst + desc[kArcOff];
+  const int *pdf = g.out_pdf + desc[kArcOff];
+  const double *p = g.out_p64 + desc[kArcOff];
+  const double *fin = g.fin64 + desc[kStateOff];
+  const double *pi = leak_pi + size_t(row) * S_max;
+  const int T = lengths[b];
+  const size_t T1 = size_t(T_max) + 1;
+  double *be = beta + size_t(b) * T1 * S_max;
+  __shared__ double s_dot;
+  {
+    const double factor = (1.0 + leak) / scales[size_t(b) * T_max + T - 1];
+    for (int s = threadIdx.x; s < S_max; s += blockDim.x)
+      be[size_t(T) * S_max + s] = __dmul_rn(s < S ? fin[s] : 0.0, factor);
+  }
+  __syncthreads();
+  for (int t = T; t >= 1; --t) {
+    const double *nxt = be + size_t(t) * S_max;
+    double *col = be + size_t(t - 1) * S_max;
+    const double *e = expl + (size_t(b) * T_max + (t - 1)) * D;
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+      double acc = 0.0;
+      for (int i = ptr[s]; i < ptr[s + 1]; ++i)
+        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(p[i], e[pdf[i]]), nxt[dst[i]]));
+      col[s] = acc;
+    }
+    __syncthreads();
+    if (t - 1 >= 1) {
+      if (leak > 0.0) {
+        if (threadIdx.x == 0) {
+          double dot = 0.0;
+          for (int s = 0; s < S_max; ++s) dot = __dadd_rn(dot, __dmul_rn(pi[s], col[s]));
+          s_dot = dot;
+        }
+        __syncthreads();
+        const double add = __dmul_rn(leak, s_dot);
+        for (int s = threadIdx.x; s < S_max; s += blockDim.x) col[s] = __dadd_rn(col[s], add);
+        __syncthreads();
+      }
+      const double inv = 1.0 / scales[size_t(b) * T_max + t - 2];
+      for (int s = threadIdx.x; s < S_max; s += blockDim.x) col[s] = __dmul_rn(col[s], inv);
+      __syncthreads();
+    }
+  }
+}
+
+// _kernels.py:194-224.  One thread per (item, frame); arcs in forward_* order.
+__global__ void post_parity_kernel(DevGraphs g, const int64_t *row_map, int B, int T_max, int D,
+                                   int S_max, const double *expl, const int *lengths,
+                                   const double *alpha, const double *beta, const int64_t *fail,
+                                   double *gamma) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= B * T_max) return;
+  const int b = u / T_max, t = u % T_max;
+  if (t >= lengths[b] || fail[b] >= 0) return;
+  const int row = int(row_map[b]);
+  const int *desc = g.desc + row * kDescInts;
+  const int I = desc[kI];
+  const int *ptr = g.out_ptr + desc[kPtrOff];
+  const int *dst = g.out_dst + desc[kArcOff];
+  const int *pdf = g.out_pdf + desc[kArcOff];
+  const double *p = g.out_p64 + desc[kArcOff];
+  const size_t T1 = size_t(T_max) + 1;
+  const double *at = alpha + (size_t(b) * T1 + t) * S_max;
+  const double *bt = beta + (size_t(b) * T1 + t + 1) * S_max;
+  const double *e = expl + (size_t(b) * T_max + t) * D;
+  double *gm = gamma + (size_t(b) * T_max + t) * D;
+  // The out-CSR is the reference forward_* order; recover from-states by row.
+  int s = 0;
+  for (int i = 0; i < I; ++i) {
+    while (ptr[s + 1] <= i) ++s;
+    const int d = pdf[i];
+    gm[d] = __dadd_rn(gm[d], __dmul_rn(__dmul_rn(__dmul_rn(at[s], p[i]), e[d]), bt[dst[i]]));
+  }
+}
+
+// Batch totals for chain_loss (loss.py:61-72), fixed-order reduction.
+__global__ void totals_kernel(int B, const int *lengths, const double *num_lp, const double *den_lp,
+                              const int *num_fail, const int *den_fail, double *totals) {
+  __shared__ double so[256], sf[256], sn[256];
+  double o = 0.0, f = 0.0, n = 0.0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (num_fail[b] < 0 && den_fail[b] < 0) {
+      o += num_lp[b] - den_lp[b];
+      f += double(lengths[b]);
+    } else {
+      n += 1.0;
+    }
+  }
+  so[threadIdx.x] = o;
+  sf[threadIdx.x] = f;
+  sn[threadIdx.x] = n;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) {
+      so[threadIdx.x] += so[threadIdx.x + w];
+      sf[threadIdx.x] += sf[threadIdx.x + w];
+      sn[threadIdx.x] += sn[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    totals[0] = so[0];
+    totals[1] = sf[0];
+    totals[2] = sn[0];
+  }
+}
+
+inline int choose_group(int max_states) {
+  const int want = (max_states + 2) / 3;
+  int g = 32;
+  while (g < want && g < 1024) g <<= 1;
+  return g;
+}
+
+template <typename Real>
+int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_max, int D,
+              const void *L, const int *lengths, double leak, double floor, const void *leak_pi,
+              void *work, size_t work_bytes, void *post, int mode, const int *other_fail,
+              double *logp, int *fail, double *scale_logs, cudaStream_t st) {
+  FBArgs<Real> a{};
+  a.g = graphs->dev;
+  a.row_map = row_map;
+  a.B = B;
+  a.T_max = T_max;
+  a.D = D;
+  a.S_max = graphs->max_states;
+  a.S_pad = pad4(graphs->max_states);
+  a.D_pad = pad4(D);
+  a.NC_pad = pad4(std::max(1, graphs->max_chunks));
+  a.T_pad = pad4(T_max);
+  a.L = static_cast<const Real *>(L);
+  a.lengths = lengths;
+  a.leak = Real(leak);
+  a.floor_eff = std::is_same<Real, float>::value ? Real(std::max(floor, double(FLT_MIN)))
+                                                 : Real(floor);
+  a.leak_pi = static_cast<const Real *>(leak_pi);
+  a.work = static_cast<Real *>(work);
+  a.post = static_cast<Real *>(post);
+  a.mode = mode;
+  a.other_fail = other_fail;
+  a.logp = logp;
+  a.fail = fail;
+  a.scale_logs = scale_logs;
+  a.I_pad = pad4(std::max(1, graphs->max_arcs));
+  if (work_bytes < size_t(a.S_pad) * sizeof(Real))
+    return set_error(LFMMI_ERR_INVALID, "workspace too small");
+  // Numerator-sized graphs: one warp per utterance.  Larger graphs: one CTA
+  // per utterance with the arc layout in shared memory.  The choice depends
+  // only on the graph batch, so an utterance's result never depends on which
+  // other utterances share its batch.
+  const bool small = graphs->max_states <= 512;
+  if (!std::getenv("LFMMI_DISABLE_TILE")) {
+    const int rc = launch_tile<Real>(a, graphs, small, st);
+    if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
+  }
+  return launch_group<Real>(a, small ? choose_group(graphs->max_states) : 1024, st);
+}
+
+}  // namespace lfmmi
+
+using namespace lfmmi;
+
+extern "C" size_t lfmmi_workspace_size(int32_t max_states, int64_t total_frames,
+                                       int32_t precision) {
+  const size_t es = precision == LFMMI_F64 ? 8 : 4;
+  return size_t(pad4(std::max(1, int(max_states)))) * size_t(std::max<int64_t>(total_frames, 1)) *
+             es + 256;
+}
+
+static int check_common(const lfmmi_graphs *graphs, int32_t batch, int32_t max_frames,
+                        int32_t num_pdfs, int32_t precision) {
+  if (!graphs) return set_error(LFMMI_ERR_INVALID, "graph handle is NULL");
+  if (batch < 1 || max_frames < 1) return set_error(LFMMI_ERR_INVALID, "empty batch");
+  if (num_pdfs != graphs->num_pdfs)
+    return set_error(LFMMI_ERR_INVALID,
+                     "pdf dimension mismatch: batch has " + std::to_string(num_pdfs) +
+                         ", graphs have " + std::to_string(graphs->num_pdfs));
+  if (precision != LFMMI_F32 && precision != LFMMI_F64)
+    return set_error(LFMMI_ERR_INVALID, "precision must be LFMMI_F32 or LFMMI_F64");
+  return LFMMI_OK;
+}
+
+extern "C" int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t *row_map,
+                                      int32_t batch, int32_t max_frames, int32_t num_pdfs,
+                                      int32_t precision, const void *loglikes,
+                                      const int32_t *lengths, double leak, double scale_floor,
+                                      const void *leak_pi, void *workspace,
+                                      size_t workspace_bytes, void *posteriors,
+                                      int32_t post_mode, const int32_t *other_fail,
+                                      double *log_probs, int32_t *fail_frames,
+                                      double *scale_logs, void *stream) {
+  int rc = check_common(graphs, batch, max_frames, num_pdfs, precision);
+  if (rc) return rc;
+  if (!row_map || !loglikes || !lengths || !workspace || !posteriors || !log_probs || !fail_frames)
+    return set_error(LFMMI_ERR_INVALID, "lfmmi_forward_backward: NULL device pointer");
+  if (post_mode < LFMMI_POST_WRITE || post_mode > LFMMI_POST_NEGATE)
+    return set_error(LFMMI_ERR_INVALID, "unknown post_mode");
+  if (!(leak >= 0.0) || !(scale_floor > 0.0))
+    return set_error(LFMMI_ERR_INVALID, "leak must be >= 0 and scale_floor > 0");
+  auto st = static_cast<cudaStream_t>(stream);
+  if (precision == LFMMI_F64)
+    return run_fused<double>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
+                             scale_floor, leak_pi, workspace, workspace_bytes, posteriors,
+                             post_mode, other_fail, log_probs, fail_frames, scale_logs, st);
+  return run_fused<float>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
+                          scale_floor, leak_pi, workspace, workspace_bytes, posteriors, post_mode,
+                          other_fail, log_probs, fail_frames, scale_logs, st);
+}
+
+extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *num_row_map,
+                                const lfmmi_graphs *denominator, const int64_t *den_row_map,
+                                int32_t batch, int32_t max_frames, int32_t num_pdfs,
+                                int32_t precision, const void *loglikes, const int32_t *lengths,
+                                double leak, double scale_floor, const void *num_leak_pi,
+                                const void *den_leak_pi, void *workspace, size_t workspace_bytes,
+                                void *grad, double *num_log_probs, double *den_log_probs,
+                                int32_t *num_fail, int32_t *den_fail, double *totals,
+                                void *stream) {
+  // Denominator first (the expensive pass writes -gamma_den without reading
+  // the gradient), then the numerator adds gamma_num and zeroes rows of items
+  // where either recursion failed (loss.py:61-69).
+  int rc = lfmmi_forward_backward(denominator, den_row_map, batch, max_frames, num_pdfs,
+                                  precision, loglikes, lengths, leak, scale_floor, den_leak_pi,
+                                  workspace, workspace_bytes, grad, LFMMI_POST_NEGATE, nullptr,
+                                  den_log_probs, den_fail, nullptr, stream);
+  if (rc) return rc;
+  rc = lfmmi_forward_backward(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
+                              loglikes, lengths, leak, scale_floor, num_leak_pi, workspace,
+                              workspace_bytes, grad, LFMMI_POST_ADD, den_fail, num_log_probs,
+                              num_fail, nullptr, stream);
+  if (rc) return rc;
+  if (totals) {
+    totals_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        batch, lengths, num_log_probs, den_log_probs, num_fail, den_fail, totals);
+    rc = check_cuda(cudaGetLastError(), "totals_kernel launch");
+  }
+  return rc;
+}
+
+extern "C" int lfmmi_forward_kernel(const lfmmi_graphs *graphs, const int64_t *row_map,
+                                    int32_t batch, int32_t max_frames, int32_t num_pdfs,
+                                    const double *expl, const int32_t *lengths, double leak,
+                                    const double *leak_pi, double scale_floor, double *alpha,
+                                    double *scales, int64_t *fail_frames, void *stream) {
+  int rc = check_common(graphs, batch, max_frames, num_pdfs, LFMMI_F64);
+  if (rc) return rc;
+  if (!leak_pi) return set_error(LFMMI_ERR_INVALID, "parity kernels need an explicit leak_pi");
+  fwd_parity_kernel<<<batch, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      graphs->dev, row_map, batch, max_frames, num_pdfs, graphs->max_states, expl, lengths, leak,
+      leak_pi, scale_floor, alpha, scales, fail_frames);
+  return check_cuda(cudaGetLastError(), "fwd_parity_kernel launch");
+}
+
+extern "C" int lfmmi_backward_kernel(const lfmmi_graphs *graphs, const int64_t *row_map,
+                                     int32_t batch, int32_t max_frames, int32_t num_pdfs,
+                                     const double *expl, const int32_t *lengths,
+                                     const double *scales, double leak, const double *leak_pi,
+                                     const int64_t *fail_frames, double *beta, void *stream) {
+  int rc = check_common(graphs, batch, max_frames, num_pdfs, LFMMI_F64);
+  if (rc) return rc;
+  if (!leak_pi) return set_error(LFMMI_ERR_INVALID, "parity kernels need an explicit leak_pi");
+  bwd_parity_kernel<<<batch, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      graphs->dev, row_map, batch, max_frames, num_pdfs, graphs->max_states, expl, lengths, scales,
+      leak, leak_pi, fail_frames, beta);
+  return check_cuda(cudaGetLastError(), "bwd_parity_kernel launch");
+}
+
+extern "C" int lfmmi_posterior_kernel(const lfmmi_graphs *graphs, const int64_t *row_map,
+                                      int32_t batch, int32_t max_frames, int32_t num_pdfs,
+                                      const double *expl, const int32_t *lengths,
+                                      const double *alpha, const double *beta,
+                                      const int64_t *fail_frames, double *gamma, void *stream) {
+  int rc = check_common(graphs, batch, max_frames, num_pdfs, LFMMI_F64);
+  if (rc) return rc;
+  const int n = batch * max_frames;
+  post_parity_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      graphs->dev, row_map, batch, max_frames, num_pdfs, graphs->max_states, expl, lengths, alpha,
+      beta, fail_frames, gamma);
+  return check_cuda(cudaGetLastError(), "post_parity_kernel launch");
+}

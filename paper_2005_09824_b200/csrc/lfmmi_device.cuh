@@ -1,0 +1,82 @@
+// Device-side helpers shared by the LF-MMI kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "lfmmi_internal.h"
+
+namespace lfmmi {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+template <typename Real>
+__device__ __forceinline__ const Real *pick(const float *f, const double *d);
+template <>
+__device__ __forceinline__ const float *pick<float>(const float *f, const double *) { return f; }
+template <>
+__device__ __forceinline__ const double *pick<double>(const float *, const double *d) { return d; }
+
+__device__ __forceinline__ float exp_r(float x) { return expf(x); }
+__device__ __forceinline__ double exp_r(double x) { return exp(x); }
+
+// ---- cp.async (LDGSTS) -----------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async_elem(float *dst, const float *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_elem(double *dst, const double *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__host__ __device__ inline int pad4(int x) { return (x + 3) & ~3; }
+
+// Kernel arguments shared by the fused kernels.
+template <typename Real>
+struct FBArgs {
+  DevGraphs g;
+  const int64_t *row_map;
+  int B, T_max, D, S_max, S_pad, D_pad, NC_pad, T_pad;
+  const Real *L;
+  const int *lengths;
+  Real leak;
+  Real floor_eff;
+  const Real *leak_pi;
+  Real *work;
+  Real *post;
+  int mode;
+  const int *other_fail;
+  double *logp;
+  int *fail;
+  double *scale_logs;
+  int I_pad;  // tile kernel: per-arc scratch (posterior slots)
+};
+
+}  // namespace lfmmi

@@ -23,7 +23,17 @@ enum DescField : int {
   kPdfPtrOff = 8,  // offset into pdf_chunk_ptr (D + 1 entries per row)
   kMaxInDeg = 9,
   kMaxOutDeg = 10,
-  kDescInts = 12
+  // tile packs (fb_tile_kernel): states sorted by degree into 32-lane tiles,
+  // arc slots stored slot-major per tile (slot j of lane l at base + 32 j + l)
+  kTileOff = 11,     // offset into per-tile arrays (trips/base), tiles = ceil(S/32)
+  kTfSlotOff = 12,   // forward (by destination) slot offset
+  kTfSlots = 13,     // forward slot count (multiple of 32)
+  kTbSlotOff = 14,   // backward (by source) slot offset
+  kTbSlots = 15,     // backward slot count
+  kPdfPtrOff2 = 16,  // offset into pdf_arc_ptr (D + 1 per row): posterior slot groups
+  kTileable = 17,    // 1 if indices fit the 16-bit tile encoding
+  kXPad = 18,        // posterior slot count incl. per-pdf padding + dummy slot (multiple of 4)
+  kDescInts = 20
 };
 
 // Device-side view of a packed graph batch (passed by value to kernels).
@@ -44,6 +54,15 @@ struct DevGraphs {
   const int *chunk_begin, *chunk_end, *chunk_pdf, *pdf_chunk_ptr;
   const float *fin32;
   const double *fin64;
+  // tile packs
+  const unsigned *tf_info, *tb_info;  // per tile lane: state | degree << 16
+  const int *tf_trips, *tf_base, *tb_trips, *tb_base;
+  const unsigned *tf_word, *tb_word;  // src|pdf<<16 (forward), dst|pdf<<16 (backward)
+  const float *tf_p32, *tb_p32;
+  const double *tf_p64, *tb_p64;
+  const unsigned short *tb_xslot;     // posterior slot of each backward arc
+  const int *pdf_arc_ptr;             // posterior slot range per pdf (16-byte aligned)
+  const uint2 *tf_wp, *tb_wp;         // interleaved (word, fp32 prob bits) slots
 };
 
 }  // namespace lfmmi
@@ -51,6 +70,8 @@ struct DevGraphs {
 struct lfmmi_graphs {
   int32_t num_rows = 0, max_states = 0, max_arcs = 0, num_pdfs = 0;
   int32_t max_chunks = 0, max_in_deg = 0, max_out_deg = 0;
+  int32_t max_tiles = 0, max_tf_slots = 0, max_tb_slots = 0, max_xpad = 0;
+  bool tileable = false;
   void *device_block = nullptr;
   size_t device_bytes = 0;
   lfmmi::DevGraphs dev{};

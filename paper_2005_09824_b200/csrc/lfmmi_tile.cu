@@ -1,0 +1,574 @@
+// Tile kernels: the LF-MMI hot path for both graph classes.
+//
+//   fb_tile_kernel<Real, 1024, 1, true>  — denominator: one 1024-thread CTA
+//       per utterance; the arc layout of the current phase is resident in
+//       shared memory (CSR-by-destination for the forward, CSR-by-source for
+//       the backward).
+//   fb_tile_kernel<Real, 32, IPC, false> — numerators: one warp per
+//       utterance (IPC utterances per CTA, __syncwarp only); the tiny
+//       per-utterance arc packs are read through L1.
+//
+// Layout: states sorted by degree into 32-lane tiles; tile w stores slot j of
+// lane l at base_w + 32 j + l, so every arc-data load is one coalesced
+// 256-byte row (word | fp32 prob interleaved) and the only random accesses
+// are the alpha/beta and emission gathers.  Padded slots carry probability 0
+// (and a dummy posterior slot), so the inner loops are branch-free.  Each
+// warp owns whole tiles: a state's sum is accumulated by one thread in CSR
+// order — deterministic, no atomics.
+//
+// Whole time loop on chip, one group barrier per frame:
+//   forward  (_kernels.py:54-122): deferred normalisation — column k+1 is
+//     gathered from the unnormalised column k and the normaliser / leaky-HMM
+//     correction of column k is applied inside the gather;
+//   backward (_kernels.py:125-191): same deferral for the leak adjoint;
+//   posterior + gradient (_kernels.py:194-224, loss.py:67-69): the backward
+//     pass already forms every arc term p * e[pdf] * beta_t[dst]; it stores
+//     alpha_{t-1}[src] * term into an owned per-arc slot grouped by pdf, and
+//     the next frame sums each pdf's slots (float4 loads) into the gradient.
+// Emissions exp(L - max_d L) (forward_backward.py:120-130) are computed on
+// the fly from log-likelihood rows staged by cp.async two frames ahead; the
+// alpha column of every frame is spilled to an HBM workspace and streamed
+// back during the backward.
+#include "lfmmi_device.cuh"
+#include "lfmmi_kernels.h"
+
+#include <string>
+
+namespace lfmmi {
+
+struct TileLayout {  // byte offsets of one utterance's slice of shared memory
+  size_t wp, xs, tinfo, ttrips, tbase, pdfptr, xterm, rbuf, aring, ebuf, stage, gstage, scales,
+      shifts, part, mpart, total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Slot storage per phase: fp32 -> uint2 (word, prob bits) [+ u16 xslot];
+// fp64 -> u32 word + f64 prob [+ u16 xslot].
+
+// Sum of n4 groups of 4 consecutive values (16/32-byte aligned), 4 accumulators.
+__device__ __forceinline__ float sum_groups4(const float *x, int n4) {
+  const float4 *q = reinterpret_cast<const float4 *>(x);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  for (int i = 0; i < n4; ++i) {
+    const float4 v = q[i];
+    s0 += v.x;
+    s1 += v.y;
+    s2 += v.z;
+    s3 += v.w;
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+__device__ __forceinline__ double sum_groups4(const double *x, int n4) {
+  const double2 *q = reinterpret_cast<const double2 *>(x);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int i = 0; i < n4; ++i) {
+    const double2 v = q[2 * i], w = q[2 * i + 1];
+    s0 += v.x;
+    s1 += v.y;
+    s2 += w.x;
+    s3 += w.y;
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+__host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int ntiles, int D,
+                                                  int X_pad, int S_pad, int D_pad, int T_pad,
+                                                  int NW, int real) {
+  TileLayout l;
+  size_t o = 512;  // scratch: 32 doubles + 32 int64
+  const size_t F = smem_graph ? size_t(Fmax) : 0;
+  const size_t nt = smem_graph ? size_t(ntiles) : 0;
+  l.wp = o;      o = al16(o + (real == 4 ? F * 8 : al16(F * 4) + F * 8));
+  l.xs = o;      o = al16(o + F * 2);
+  l.tinfo = o;   o = al16(o + nt * 32 * 4);
+  l.ttrips = o;  o = al16(o + size_t(pad4(int(nt))) * 4);
+  l.tbase = o;   o = al16(o + size_t(pad4(int(nt))) * 4);
+  l.pdfptr = o;  o = al16(o + size_t(D + 1) * 4);
+  l.xterm = o;   o = al16(o + size_t(2) * X_pad * real);
+  l.rbuf = o;    o = al16(o + size_t(2) * S_pad * real);
+  l.aring = o;   o = al16(o + size_t(2) * S_pad * real);
+  l.ebuf = o;    o = al16(o + size_t(2) * D_pad * real);
+  l.stage = o;   o = al16(o + size_t(4) * D_pad * real);
+  l.gstage = o;  o = al16(o + size_t(2) * D_pad * real);
+  l.scales = o;  o = al16(o + size_t(T_pad) * real);
+  l.shifts = o;  o = al16(o + size_t(T_pad) * real);
+  l.part = o;    o = al16(o + size_t(2) * 32 * real);
+  l.mpart = o;   o = al16(o + size_t(2) * 32 * real);
+  l.total = o;
+  (void)NW;
+  return l;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ void copy16(void *dst, const void *src, size_t bytes, int tid) {
+  const char *s = static_cast<const char *>(src);
+  char *d = static_cast<char *>(dst);
+  for (size_t c = size_t(tid) * 16; c < bytes; c += size_t(BLOCK) * 16) cp_async_16(d + c, s + c);
+}
+
+template <int GROUP, int IPC>
+__device__ __forceinline__ void tsync() {
+  if constexpr (GROUP == 32) {
+    __syncwarp();
+  } else {
+    static_assert(IPC == 1, "CTA-sized groups run one utterance per CTA");
+    __syncthreads();
+  }
+}
+
+// Sum of the first n (<= 32) entries of v, identical in every lane.
+template <typename Real>
+__device__ __forceinline__ Real lane_sum(const Real *v, int n, int lane) {
+  Real x = lane < n ? v[lane] : Real(0);
+  return warp_sum(x);
+}
+
+struct SlotF32 {
+  const uint2 *wp;
+  __device__ __forceinline__ void load(int slot, unsigned &w, float &p) const {
+    const uint2 v = wp[slot];
+    w = v.x;
+    p = __uint_as_float(v.y);
+  }
+};
+struct SlotF64 {
+  const unsigned *w;
+  const double *p;
+  __device__ __forceinline__ void load(int slot, unsigned &ww, double &pp) const {
+    ww = w[slot];
+    pp = p[slot];
+  }
+};
+template <typename Real>
+struct SlotOf;
+template <>
+struct SlotOf<float> { using type = SlotF32; };
+template <>
+struct SlotOf<double> { using type = SlotF64; };
+
+template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH>
+__global__ void __launch_bounds__(GROUP *IPC, 1)
+    fb_tile_kernel(const FBArgs<Real> a, int Fmax, int ntiles_max, int X_pad) {
+  constexpr int NW = GROUP / 32;
+  using Slot = typename SlotOf<Real>::type;
+  extern __shared__ __align__(16) unsigned char smem_all[];
+  const int gid = threadIdx.x / GROUP;
+  const int tid = threadIdx.x % GROUP, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x * IPC + gid;
+  if (b >= a.B) return;  // whole group exits together (no CTA-wide barriers for IPC > 1)
+  const TileLayout lay = tile_layout(SMEM_GRAPH, Fmax, ntiles_max, a.D, X_pad, a.S_pad, a.D_pad,
+                                     a.T_pad, NW, int(sizeof(Real)));
+  unsigned char *smem = smem_all + lay.total * gid;
+  double *dscr = reinterpret_cast<double *>(smem);
+  long long *lscr = reinterpret_cast<long long *>(smem + 256);
+  int *pdfptr = reinterpret_cast<int *>(smem + lay.pdfptr);
+  Real *xterm = reinterpret_cast<Real *>(smem + lay.xterm);
+  Real *rbuf = reinterpret_cast<Real *>(smem + lay.rbuf);
+  Real *aring = reinterpret_cast<Real *>(smem + lay.aring);
+  Real *ebuf = reinterpret_cast<Real *>(smem + lay.ebuf);
+  Real *stage = reinterpret_cast<Real *>(smem + lay.stage);
+  Real *gstage = reinterpret_cast<Real *>(smem + lay.gstage);
+  Real *scales = reinterpret_cast<Real *>(smem + lay.scales);
+  Real *shifts = reinterpret_cast<Real *>(smem + lay.shifts);
+  Real *part = reinterpret_cast<Real *>(smem + lay.part);
+  Real *mpart = reinterpret_cast<Real *>(smem + lay.mpart);
+  auto gsync = [] { tsync<GROUP, IPC>(); };
+
+  const int T = a.lengths[b];
+  const int D = a.D;
+  const int S_pad = a.S_pad, D_pad = a.D_pad;
+  const int row = int(a.row_map[b]);
+  const int *desc = a.g.desc + row * kDescInts;
+  const int S = desc[kS], init = desc[kInit];
+  const int ntiles = (S + 31) / 32;
+  const int toff = desc[kTileOff];
+  const Real *fin = pick<Real>(a.g.fin32, a.g.fin64) + desc[kStateOff];
+  const Real *Lb = a.L + size_t(b) * a.T_max * D;
+  Real *post_b = a.post + size_t(b) * a.T_max * D;
+  const int mode = a.mode;
+  const bool reads_post = mode == kPostAdd || mode == kPostSubtract;
+  const bool other_failed = a.other_fail != nullptr && a.other_fail[b] >= 0;
+  const int nrw = (D + 31) / 32 < NW ? (D + 31) / 32 : NW;  // warps holding row elements
+
+  // Arc-pack views of the current phase: shared memory (denominator) or L1 (numerators).
+  const unsigned *tinfo;
+  const int *ttrips, *tbase;
+  Slot slot;
+  const unsigned short *XS;
+  auto bind_phase = [&](bool fwd) {
+    const int so = desc[fwd ? kTfSlotOff : kTbSlotOff], nsl = desc[fwd ? kTfSlots : kTbSlots];
+    const uint2 *gwp = (fwd ? a.g.tf_wp : a.g.tb_wp) + so;
+    const unsigned *gw = (fwd ? a.g.tf_word : a.g.tb_word) + so;
+    const double *gp = (fwd ? a.g.tf_p64 : a.g.tb_p64) + so;
+    const unsigned *gi = (fwd ? a.g.tf_info : a.g.tb_info) + size_t(toff) * 32;
+    const int *gt = (fwd ? a.g.tf_trips : a.g.tb_trips) + toff;
+    const int *gb = (fwd ? a.g.tf_base : a.g.tb_base) + toff;
+    const unsigned short *gx = a.g.tb_xslot + so;
+    if constexpr (SMEM_GRAPH) {
+      unsigned char *wpb = smem + lay.wp;
+      if constexpr (sizeof(Real) == 4) {
+        copy16<GROUP>(wpb, gwp, size_t(nsl) * 8, tid);
+        slot.wp = reinterpret_cast<const uint2 *>(wpb);
+      } else {
+        unsigned *w = reinterpret_cast<unsigned *>(wpb);
+        double *p = reinterpret_cast<double *>(wpb + al16(size_t(Fmax) * 4));
+        copy16<GROUP>(w, gw, size_t(nsl) * 4, tid);
+        copy16<GROUP>(p, gp, size_t(nsl) * 8, tid);
+        slot.w = w;
+        slot.p = p;
+      }
+      unsigned short *xs = reinterpret_cast<unsigned short *>(smem + lay.xs);
+      if (!fwd) copy16<GROUP>(xs, gx, size_t(nsl) * 2, tid);
+      XS = xs;
+      unsigned *ti = reinterpret_cast<unsigned *>(smem + lay.tinfo);
+      int *tt = reinterpret_cast<int *>(smem + lay.ttrips);
+      int *tb = reinterpret_cast<int *>(smem + lay.tbase);
+      copy16<GROUP>(ti, gi, size_t(ntiles) * 128, tid);
+      copy16<GROUP>(tt, gt, size_t(pad4(ntiles)) * 4, tid);
+      copy16<GROUP>(tb, gb, size_t(pad4(ntiles)) * 4, tid);
+      tinfo = ti;
+      ttrips = tt;
+      tbase = tb;
+    } else {
+      if constexpr (sizeof(Real) == 4) {
+        slot.wp = gwp;
+      } else {
+        slot.w = gw;
+        slot.p = gp;
+      }
+      XS = gx;
+      tinfo = gi;
+      ttrips = gt;
+      tbase = gb;
+    }
+  };
+  bind_phase(true);
+
+  long long off = 0;
+  for (int j = tid; j < b; j += GROUP) off += a.lengths[j];
+  off = warp_sum(off);
+  const Real *pi = a.leak_pi ? a.leak_pi + size_t(row) * a.S_max : nullptr;
+  double psum_d = 0.0;
+  if (pi)
+    for (int s = tid; s < S; s += GROUP) psum_d += double(pi[s]);
+  psum_d = warp_sum(psum_d);
+  if (lane == 0) {
+    lscr[warp] = off;
+    dscr[warp] = psum_d;
+  }
+  gsync();
+  long long item_off = 0;
+  double pisum_d = 0.0;
+  for (int w = 0; w < NW; ++w) {
+    item_off += lscr[w];
+    pisum_d += dscr[w];
+  }
+  const Real upi = Real(1.0 / double(S));
+  const Real pisum = pi ? Real(pisum_d) : Real(1);
+  const Real lam = a.leak;
+  Real *trellis = a.work + item_off * S_pad;
+
+  if (!reads_post) {
+    const size_t n = size_t(a.T_max - T) * D;
+    for (size_t i = tid; i < n; i += GROUP) post_b[size_t(T) * D + i] = Real(0);
+  }
+
+  auto issue_row = [&](int t) {
+    if (t < 0 || t >= T) return;
+    const Real *src = Lb + size_t(t) * D;
+    Real *dst = stage + (t & 3) * D_pad;
+    for (int d = tid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
+  };
+  auto row_max_part = [&](int t) {
+    if (t < 0 || t >= T || warp >= nrw) return;
+    const Real *src = stage + (t & 3) * D_pad;
+    Real m = -INFINITY;
+    for (int d = tid; d < D; d += GROUP) m = fmax(m, src[d]);
+    m = warp_max(m);
+    if (lane == 0) mpart[(t & 1) * 32 + warp] = m;
+  };
+  auto compute_e = [&](int t, bool record_shift) {
+    const Real *mp = mpart + (t & 1) * 32;
+    Real m = lane < nrw ? mp[lane] : Real(-INFINITY);
+    m = warp_max(m);
+    const Real *src = stage + (t & 3) * D_pad;
+    Real *dst = ebuf + (t & 1) * D_pad;
+    for (int d = tid; d < D; d += GROUP) dst[d] = exp_r(src[d] - m);
+    if (record_shift && tid == 0) shifts[t] = m;
+  };
+
+  // ---- prologue -----------------------------------------------------------------
+  for (int s = tid; s < S; s += GROUP) rbuf[s] = (s == init) ? Real(1) : Real(0);
+  issue_row(0);
+  issue_row(1);
+  cp_async_commit();
+  cp_async_wait<0>();
+  row_max_part(0);
+  row_max_part(1);
+  gsync();
+  compute_e(0, true);
+  gsync();
+
+  // ---- forward: one barrier per frame ------------------------------------------------
+  Real inv2 = Real(1), leakc = Real(0);
+  int fail_at = -1;
+  for (int k = 0; k < T; ++k) {
+    const int cur = k & 1, nxt = cur ^ 1;
+    if (k > 0) {
+      const Real t0 = lane_sum(part + cur * 32, NW, lane);
+      Real t2 = t0;
+      leakc = Real(0);
+      if (lam > Real(0) && t0 > Real(0)) {
+        leakc = lam * t0;
+        t2 = t0 + leakc * pisum;
+      }
+      if (!(t2 >= a.floor_eff) || isinf(t2)) {
+        fail_at = k - 1;
+        break;
+      }
+      inv2 = Real(1) / t2;
+      if (tid == 0) scales[k - 1] = t2;
+    }
+    {
+      const Real *r = rbuf + cur * S_pad;
+      Real *arow = trellis + size_t(k) * S_pad;
+      for (int s = tid; s < S; s += GROUP) arow[s] = (r[s] + leakc * (pi ? pi[s] : upi)) * inv2;
+    }
+    if (k + 1 < T) compute_e(k + 1, true);
+    issue_row(k + 2);
+    cp_async_commit();
+    {
+      const Real *e = ebuf + cur * D_pad;
+      const Real *r = rbuf + cur * S_pad;
+      Real *rn = rbuf + nxt * S_pad;
+      const bool last = (k + 1 == T);
+      Real psum = Real(0);
+      for (int tile = warp; tile < ntiles; tile += NW) {
+        const unsigned info = tinfo[tile * 32 + lane];
+        const int trips = ttrips[tile];
+        const int base = tbase[tile] + lane;
+        Real A = Real(0), Bs = Real(0);
+        if (leakc != Real(0)) {
+#pragma unroll 4
+          for (int j = 0; j < trips; ++j) {
+            unsigned wd;
+            Real p;
+            slot.load(base + 32 * j, wd, p);
+            const Real w = p * e[wd >> 16];
+            const int src = int(wd & 0xFFFFu);
+            A = fma(w, r[src], A);
+            Bs = pi ? fma(w, pi[src], Bs) : Bs + w;
+          }
+        } else {
+#pragma unroll 4
+          for (int j = 0; j < trips; ++j) {
+            unsigned wd;
+            Real p;
+            slot.load(base + 32 * j, wd, p);
+            A = fma(p * e[wd >> 16], r[wd & 0xFFFFu], A);
+          }
+        }
+        const int s = int(info & 0xFFFFu);
+        if (s != 0xFFFF) {
+          Real raw = inv2 * (A + leakc * (pi ? Bs : upi * Bs));
+          if (last) raw *= fin[s];
+          rn[s] = raw;
+          psum += raw;
+        }
+      }
+      psum = warp_sum(psum);
+      if (lane == 0) part[nxt * 32 + warp] = psum;
+    }
+    cp_async_wait<0>();
+    row_max_part(k + 2);
+    gsync();
+  }
+  if (fail_at < 0) {
+    const Real t0 = lane_sum(part + (T & 1) * 32, NW, lane);
+    Real t2 = t0;
+    if (lam > Real(0) && t0 > Real(0)) t2 = t0 + lam * t0 * pisum;
+    if (!(t2 >= a.floor_eff) || isinf(t2))
+      fail_at = T - 1;
+    else if (tid == 0)
+      scales[T - 1] = t2;
+  }
+  if (fail_at >= 0) {
+    // The reference exponentiates every valid frame: remaining shifts are row
+    // maxima, remaining scales stay 1 (forward_backward.py:184,206).
+    for (int k = fail_at + 1 + warp; k < T; k += NW) {
+      Real m = -INFINITY;
+      for (int d = lane; d < D; d += 32) m = fmax(m, Lb[size_t(k) * D + d]);
+      m = warp_max(m);
+      if (lane == 0) shifts[k] = m;
+    }
+    for (int k = fail_at + tid; k < T; k += GROUP) scales[k] = Real(1);
+  }
+  gsync();
+  {
+    double acc = 0.0;
+    for (int k = tid; k < T; k += GROUP) {
+      const double v = log(double(scales[k])) + double(shifts[k]);
+      acc += v;
+      if (a.scale_logs) a.scale_logs[size_t(b) * a.T_max + k] = v;
+    }
+    if (a.scale_logs)
+      for (int k = T + tid; k < a.T_max; k += GROUP) a.scale_logs[size_t(b) * a.T_max + k] = 0.0;
+    acc = warp_sum(acc);
+    if (lane == 0) dscr[warp] = acc;
+    gsync();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < NW; ++w) tot += dscr[w];
+      a.logp[b] = fail_at >= 0 ? NAN : tot;
+      a.fail[b] = fail_at;
+    }
+  }
+  if (fail_at >= 0 || other_failed) {
+    const size_t n = size_t(T) * D;
+    for (size_t i = tid; i < n; i += GROUP) post_b[i] = Real(0);
+    return;
+  }
+
+  // ---- backward + fused posterior / gradient ---------------------------------------
+  bind_phase(false);
+  {
+    const int *pp = a.g.pdf_arc_ptr + desc[kPdfPtrOff2];
+    for (int d = tid; d <= D; d += GROUP) pdfptr[d] = pp[d];
+    // Padding slots of the per-pdf groups are never written: zero them once.
+    for (int i = tid; i < 2 * X_pad; i += GROUP) xterm[i] = Real(0);
+  }
+  auto issue_alpha = [&](int k) {
+    if (k < 0) return;
+    copy16<GROUP>(aring + (k & 1) * S_pad, trellis + size_t(k) * S_pad,
+                  size_t(S_pad) * sizeof(Real), tid);
+  };
+  auto issue_post = [&](int t) {
+    if (!reads_post || t < 0 || t >= T) return;
+    const Real *src = post_b + size_t(t) * D;
+    Real *dst = gstage + (t & 1) * D_pad;
+    for (int d = tid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
+  };
+  // gamma_t[d] = sum of pdf d's slots (float4 loads, 4 accumulators).
+  auto flush_post = [&](int t, const Real *xt) {
+    Real *prow = post_b + size_t(t) * D;
+    const Real *old = gstage + (t & 1) * D_pad;
+    for (int d = tid; d < D; d += GROUP) {
+      const Real g = sum_groups4(xt + pdfptr[d], (pdfptr[d + 1] - pdfptr[d]) >> 2);
+      switch (mode) {
+        case kPostNegate: prow[d] = -g; break;
+        case kPostAdd: prow[d] = old[d] + g; break;
+        case kPostSubtract: prow[d] = old[d] - g; break;
+        default: prow[d] = g;
+      }
+    }
+  };
+
+  for (int s = tid; s < S; s += GROUP) rbuf[(T & 1) * S_pad + s] = fin[s] * (Real(1) + lam);
+  issue_row(T - 1);
+  issue_row(T - 2);
+  issue_alpha(T - 1);
+  cp_async_commit();
+  cp_async_wait<0>();
+  row_max_part(T - 1);
+  row_max_part(T - 2);
+  gsync();
+  compute_e(T - 1, false);
+  gsync();
+
+  for (int t = T; t >= 1; --t) {
+    const int ct = t & 1, cp = ct ^ 1;
+    Real ld = Real(0);
+    if (t < T && lam > Real(0)) ld = lam * lane_sum(part + ct * 32, NW, lane);
+    const Real inv = Real(1) / scales[t - 1];
+    if (t < T) flush_post(t, xterm + ct * X_pad);
+    if (t - 2 >= 0) compute_e(t - 2, false);
+    issue_row(t - 3);
+    issue_alpha(t - 2);
+    issue_post(t - 1);
+    cp_async_commit();
+    {
+      const Real *bt = rbuf + ct * S_pad;
+      const Real *e = ebuf + cp * D_pad;
+      const Real *al = aring + cp * S_pad;  // alpha_{t-1}
+      Real *bn = rbuf + cp * S_pad;
+      Real *xt = xterm + cp * X_pad;
+      Real dp = Real(0);
+      for (int tile = warp; tile < ntiles; tile += NW) {
+        const unsigned info = tinfo[tile * 32 + lane];
+        const int trips = ttrips[tile];
+        const int base = tbase[tile] + lane;
+        const int s = int(info & 0xFFFFu);
+        const Real as = (s != 0xFFFF) ? al[s] * inv : Real(0);
+        Real A = Real(0);
+#pragma unroll 4
+        for (int j = 0; j < trips; ++j) {
+          unsigned wd;
+          Real p;
+          slot.load(base + 32 * j, wd, p);
+          const Real term = p * e[wd >> 16] * (bt[wd & 0xFFFFu] + ld);
+          A += term;
+          xt[XS[base + 32 * j]] = as * term;
+        }
+        if (s != 0xFFFF) {
+          const Real v = inv * A;
+          bn[s] = v;
+          dp = fma(pi ? pi[s] : upi, v, dp);
+        }
+      }
+      dp = warp_sum(dp);
+      if (lane == 0) part[cp * 32 + warp] = dp;
+    }
+    cp_async_wait<0>();
+    row_max_part(t - 3);
+    gsync();
+  }
+  flush_post(0, xterm);
+}
+
+template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH>
+static int launch_tile_impl(const FBArgs<Real> &a, const lfmmi_graphs *g, size_t per_item,
+                            cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    int rc = check_cuda(cudaFuncSetAttribute(fb_tile_kernel<Real, GROUP, IPC, SMEM_GRAPH>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
+                        "cudaFuncSetAttribute(tile)");
+    if (rc) return rc;
+    configured = true;
+  }
+  const int grid = (a.B + IPC - 1) / IPC;
+  const int Fmax = std::max(g->max_tf_slots, g->max_tb_slots);
+  fb_tile_kernel<Real, GROUP, IPC, SMEM_GRAPH><<<grid, GROUP * IPC, per_item * IPC, st>>>(
+      a, Fmax, g->max_tiles, pad4(std::max(4, g->max_xpad)));
+  return check_cuda(cudaGetLastError(), "fb_tile_kernel launch");
+}
+
+template <typename Real>
+int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item,
+                cudaStream_t st) {
+  if (!g->tileable) return set_error(LFMMI_ERR_UNSUPPORTED, "graph not tileable");
+  const int Fmax = std::max(g->max_tf_slots, g->max_tb_slots);
+  const int X_pad = pad4(std::max(4, g->max_xpad));
+  const int real = int(sizeof(Real));
+  if (warp_per_item) {
+    const size_t per = tile_layout(false, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
+                                   a.T_pad, 1, real).total;
+    if (per * 8 <= size_t(kMaxSmem)) return launch_tile_impl<Real, 32, 8, false>(a, g, per, st);
+    if (per * 2 <= size_t(kMaxSmem)) return launch_tile_impl<Real, 32, 2, false>(a, g, per, st);
+    if (per <= size_t(kMaxSmem)) return launch_tile_impl<Real, 32, 1, false>(a, g, per, st);
+    return set_error(LFMMI_ERR_UNSUPPORTED, "numerator slice exceeds shared memory");
+  }
+  const size_t per = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
+                                 a.T_pad, 32, real).total;
+  if (per > size_t(kMaxSmem))
+    return set_error(LFMMI_ERR_UNSUPPORTED,
+                     "tile pack needs " + std::to_string(per) + " B shared memory");
+  return launch_tile_impl<Real, 1024, 1, true>(a, g, per, st);
+}
+
+template int launch_tile<float>(const FBArgs<float> &, const lfmmi_graphs *, bool, cudaStream_t);
+template int launch_tile<double>(const FBArgs<double> &, const lfmmi_graphs *, bool,
+                                 cudaStream_t);
+
+}  // namespace lfmmi

@@ -116,9 +116,12 @@ def test_three_phase_api(cuda, name):
 
 
 # ------------------------------------------------- BASELINE configs vs oracle
+@pytest.mark.parametrize("kernel", ["auto", "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
                                                ("wsj_biphone", 4), ("sweep", 6)])
-def test_configs_vs_oracle(cuda, config, batch_size):
+def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
+    if kernel == "group":  # force the generic group kernel for the denominator
+        monkeypatch.setenv("LFMMI_DISABLE_TILE", "1")
     w = synth.make_workload(config, seed=3, batch_size=batch_size)
     batch, nums, den = w.build(P)
     res = P.chain_loss(batch, nums, den)
