@@ -104,11 +104,21 @@ int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t *row_map, i
                            const int32_t *other_fail, double *log_probs, int32_t *fail_frames,
                            double *scale_logs, void *stream);
 
+/* Workspace bytes for lfmmi_chain_loss (both trellises + numerator posteriors). */
+size_t lfmmi_chain_loss_workspace_size(const lfmmi_graphs *numerators,
+                                       const lfmmi_graphs *denominator, int32_t batch,
+                                       int32_t max_frames, int32_t num_pdfs,
+                                       int64_t total_frames, int32_t precision);
+
 /*
- * LF-MMI objective and gradient for one batch (loss.py:42-84): denominator pass
- * (NEGATE) then numerator pass (ADD) into `grad`, then a reduction of
+ * LF-MMI objective and gradient for one batch (loss.py:42-84).  The numerator
+ * pass (posteriors into the workspace) runs on an internal auxiliary stream
+ * concurrently with the denominator pass (grad = -gamma_den); a combine step
+ * adds gamma_num and zeroes rows of items where either recursion failed
+ * (loss.py:61-69), then a reduction writes
  * totals[0] = sum_ok(num_lp - den_lp), totals[1] = sum_ok(T_b),
  * totals[2] = #failed   (device f64[3]; sum-reducible across ranks).
+ * All work is ordered after prior work on `stream` and before later work on it.
  */
 int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *num_row_map,
                      const lfmmi_graphs *denominator, const int64_t *den_row_map, int32_t batch,

@@ -312,6 +312,69 @@ extern "C" int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t 
                           other_fail, log_probs, fail_frames, scale_logs, st);
 }
 
+// Bytes of workspace for lfmmi_chain_loss: both alpha trellises (the two
+// passes run concurrently) + the numerator posteriors.
+static size_t chain_ws_parts(const lfmmi_graphs *num, const lfmmi_graphs *den, int32_t batch,
+                             int32_t max_frames, int32_t num_pdfs, int64_t total_frames,
+                             int32_t precision, size_t *den_off, size_t *num_off,
+                             size_t *gam_off) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t es = precision == LFMMI_F64 ? 8 : 4;
+  const size_t tf = size_t(std::max<int64_t>(total_frames, 1));
+  const size_t den_b = al(size_t(pad4(den ? den->max_states : 1)) * tf * es);
+  const size_t num_b = al(size_t(pad4(num ? num->max_states : 1)) * tf * es);
+  const size_t gam_b = al(size_t(batch) * size_t(max_frames) * size_t(num_pdfs) * es);
+  if (den_off) *den_off = 0;
+  if (num_off) *num_off = den_b;
+  if (gam_off) *gam_off = den_b + num_b;
+  return den_b + num_b + gam_b + 256;
+}
+
+extern "C" size_t lfmmi_chain_loss_workspace_size(const lfmmi_graphs *numerators,
+                                                  const lfmmi_graphs *denominator, int32_t batch,
+                                                  int32_t max_frames, int32_t num_pdfs,
+                                                  int64_t total_frames, int32_t precision) {
+  return chain_ws_parts(numerators, denominator, batch, max_frames, num_pdfs, total_frames,
+                        precision, nullptr, nullptr, nullptr);
+}
+
+// grad = (ok ? grad + gamma_num : 0) over valid rows; padded rows were zeroed
+// by the denominator pass.  Float4-vectorised grid-stride loop.
+template <typename Real>
+__global__ void combine_kernel(int B, int T_max, int D, const int *lengths, const int *num_fail,
+                               const int *den_fail, const Real *__restrict__ gnum,
+                               Real *__restrict__ grad) {
+  const size_t row_elems = size_t(T_max) * D;
+  for (int b = blockIdx.y; b < B; b += gridDim.y) {
+    const size_t n = size_t(lengths[b]) * D;
+    const bool ok = num_fail[b] < 0 && den_fail[b] < 0;
+    Real *g = grad + size_t(b) * row_elems;
+    const Real *q = gnum + size_t(b) * row_elems;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+      g[i] = ok ? g[i] + q[i] : Real(0);
+  }
+}
+
+namespace {
+struct AuxStream {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+AuxStream &aux_for_device() {
+  static AuxStream per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  AuxStream &a = per_dev[dev & 63];
+  if (!a.aux) {
+    cudaStreamCreateWithFlags(&a.aux, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming);
+  }
+  return a;
+}
+}  // namespace
+
 extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *num_row_map,
                                 const lfmmi_graphs *denominator, const int64_t *den_row_map,
                                 int32_t batch, int32_t max_frames, int32_t num_pdfs,
@@ -321,22 +384,66 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
                                 void *grad, double *num_log_probs, double *den_log_probs,
                                 int32_t *num_fail, int32_t *den_fail, double *totals,
                                 void *stream) {
-  // Denominator first (the expensive pass writes -gamma_den without reading
-  // the gradient), then the numerator adds gamma_num and zeroes rows of items
-  // where either recursion failed (loss.py:61-69).
-  int rc = lfmmi_forward_backward(denominator, den_row_map, batch, max_frames, num_pdfs,
-                                  precision, loglikes, lengths, leak, scale_floor, den_leak_pi,
-                                  workspace, workspace_bytes, grad, LFMMI_POST_NEGATE, nullptr,
-                                  den_log_probs, den_fail, nullptr, stream);
+  if (!numerators || !denominator)
+    return set_error(LFMMI_ERR_INVALID, "lfmmi_chain_loss: NULL graph handle");
+  // Total frames bound the trellis; the caller sized the workspace with
+  // lfmmi_chain_loss_workspace_size for its sum of lengths, which we recover
+  // from the byte count.
+  size_t den_off, num_off, gam_off;
+  const size_t es = precision == LFMMI_F64 ? 8 : 4;
+  const size_t gam_b = size_t(batch) * size_t(max_frames) * size_t(num_pdfs) * es;
+  const size_t per_frame =
+      size_t(pad4(denominator->max_states) + pad4(numerators->max_states)) * es;
+  if (workspace_bytes < gam_b + per_frame + 1024)
+    return set_error(LFMMI_ERR_INVALID, "chain_loss workspace too small");
+  const int64_t frames_cap = int64_t((workspace_bytes - gam_b - 1024) / per_frame);
+  chain_ws_parts(numerators, denominator, batch, max_frames, num_pdfs, frames_cap, precision,
+                 &den_off, &num_off, &gam_off);
+  char *ws = static_cast<char *>(workspace);
+  const size_t num_bytes = gam_off - num_off, den_bytes = num_off - den_off;
+  auto st = static_cast<cudaStream_t>(stream);
+  AuxStream &ax = aux_for_device();
+  // Fork: the numerator pass (small graphs, latency-bound, one warp per
+  // utterance) runs on the auxiliary stream next to the denominator pass (one
+  // CTA per utterance).  The denominator is launched first so its CTAs claim
+  // whole SMs; the numerator warps fill the SMs it leaves free.
+  int rc = check_cuda(cudaEventRecord(ax.fork, st), "cudaEventRecord(fork)");
+  if (rc) return rc;
+  rc = lfmmi_forward_backward(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
+                              loglikes, lengths, leak, scale_floor, den_leak_pi, ws + den_off,
+                              den_bytes, grad, LFMMI_POST_NEGATE, nullptr, den_log_probs,
+                              den_fail, nullptr, stream);
+  if (rc) return rc;
+  rc = check_cuda(cudaStreamWaitEvent(ax.aux, ax.fork, 0), "cudaStreamWaitEvent(fork)");
   if (rc) return rc;
   rc = lfmmi_forward_backward(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
-                              loglikes, lengths, leak, scale_floor, num_leak_pi, workspace,
-                              workspace_bytes, grad, LFMMI_POST_ADD, den_fail, num_log_probs,
-                              num_fail, nullptr, stream);
+                              loglikes, lengths, leak, scale_floor, num_leak_pi, ws + num_off,
+                              num_bytes, ws + gam_off, LFMMI_POST_WRITE, nullptr, num_log_probs,
+                              num_fail, nullptr, ax.aux);
   if (rc) return rc;
+  rc = check_cuda(cudaEventRecord(ax.join, ax.aux), "cudaEventRecord(join)");
+  if (rc) return rc;
+  rc = check_cuda(cudaStreamWaitEvent(st, ax.join, 0), "cudaStreamWaitEvent(join)");
+  if (rc) return rc;
+  {
+    const dim3 grid(std::max(1, std::min(32, (max_frames * num_pdfs + 1023) / 1024)),
+                    std::min(batch, 4096));
+    if (precision == LFMMI_F64)
+      combine_kernel<double><<<grid, 256, 0, st>>>(batch, max_frames, num_pdfs, lengths, num_fail,
+                                                   den_fail,
+                                                   reinterpret_cast<const double *>(ws + gam_off),
+                                                   static_cast<double *>(grad));
+    else
+      combine_kernel<float><<<grid, 256, 0, st>>>(batch, max_frames, num_pdfs, lengths, num_fail,
+                                                  den_fail,
+                                                  reinterpret_cast<const float *>(ws + gam_off),
+                                                  static_cast<float *>(grad));
+    rc = check_cuda(cudaGetLastError(), "combine_kernel launch");
+    if (rc) return rc;
+  }
   if (totals) {
-    totals_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        batch, lengths, num_log_probs, den_log_probs, num_fail, den_fail, totals);
+    totals_kernel<<<1, 256, 0, st>>>(batch, lengths, num_log_probs, den_log_probs, num_fail,
+                                     den_fail, totals);
     rc = check_cuda(cudaGetLastError(), "totals_kernel launch");
   }
   return rc;

@@ -117,11 +117,15 @@ __device__ __forceinline__ void tsync() {
   }
 }
 
-// Sum of the first n (<= 32) entries of v, identical in every lane.
-template <typename Real>
-__device__ __forceinline__ Real lane_sum(const Real *v, int n, int lane) {
-  Real x = lane < n ? v[lane] : Real(0);
-  return warp_sum(x);
+// Sum of the NW (<= 32) per-warp partials in v, identical in every lane.
+template <int NW, typename Real>
+__device__ __forceinline__ Real lane_sum(const Real *v, int lane) {
+  if constexpr (NW == 1) {
+    return v[0];
+  } else {
+    Real x = lane < NW ? v[lane] : Real(0);
+    return warp_sum(x);
+  }
 }
 
 struct SlotF32 {
@@ -290,8 +294,13 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   };
   auto compute_e = [&](int t, bool record_shift) {
     const Real *mp = mpart + (t & 1) * 32;
-    Real m = lane < nrw ? mp[lane] : Real(-INFINITY);
-    m = warp_max(m);
+    Real m;
+    if constexpr (NW == 1) {
+      m = mp[0];
+    } else {
+      m = lane < nrw ? mp[lane] : Real(-INFINITY);
+      m = warp_max(m);
+    }
     const Real *src = stage + (t & 3) * D_pad;
     Real *dst = ebuf + (t & 1) * D_pad;
     for (int d = tid; d < D; d += GROUP) dst[d] = exp_r(src[d] - m);
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   for (int k = 0; k < T; ++k) {
     const int cur = k & 1, nxt = cur ^ 1;
     if (k > 0) {
-      const Real t0 = lane_sum(part + cur * 32, NW, lane);
+      const Real t0 = lane_sum<NW>(part + cur * 32, lane);
       Real t2 = t0;
       leakc = Real(0);
       if (lam > Real(0) && t0 > Real(0)) {
@@ -385,7 +394,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     gsync();
   }
   if (fail_at < 0) {
-    const Real t0 = lane_sum(part + (T & 1) * 32, NW, lane);
+    const Real t0 = lane_sum<NW>(part + (T & 1) * 32, lane);
     Real t2 = t0;
     if (lam > Real(0) && t0 > Real(0)) t2 = t0 + lam * t0 * pisum;
     if (!(t2 >= a.floor_eff) || isinf(t2))
@@ -479,7 +488,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   for (int t = T; t >= 1; --t) {
     const int ct = t & 1, cp = ct ^ 1;
     Real ld = Real(0);
-    if (t < T && lam > Real(0)) ld = lam * lane_sum(part + ct * 32, NW, lane);
+    if (t < T && lam > Real(0)) ld = lam * lane_sum<NW>(part + ct * 32, lane);
     const Real inv = Real(1) / scales[t - 1];
     if (t < T) flush_post(t, xterm + ct * X_pad);
     if (t - 2 >= 0) compute_e(t - 2, false);
@@ -554,8 +563,15 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
   if (warp_per_item) {
     const size_t per = tile_layout(false, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
                                    a.T_pad, 1, real).total;
-    if (per * 8 <= size_t(kMaxSmem)) return launch_tile_impl<Real, 32, 8, false>(a, g, per, st);
-    if (per * 2 <= size_t(kMaxSmem)) return launch_tile_impl<Real, 32, 2, false>(a, g, per, st);
+    // Several utterances per CTA, but keep at least ~one CTA per SM busy.
+    const size_t per_s = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
+                                     a.T_pad, 1, real).total;
+    const bool many = a.B >= 8 * 148;
+    if (many && per_s * 8 <= size_t(kMaxSmem))
+      return launch_tile_impl<Real, 32, 8, true>(a, g, per_s, st);
+    if (per_s * 2 <= size_t(kMaxSmem) && a.B >= 2 * 148)
+      return launch_tile_impl<Real, 32, 2, true>(a, g, per_s, st);
+    if (per_s <= size_t(kMaxSmem)) return launch_tile_impl<Real, 32, 1, true>(a, g, per_s, st);
     if (per <= size_t(kMaxSmem)) return launch_tile_impl<Real, 32, 1, false>(a, g, per, st);
     return set_error(LFMMI_ERR_UNSUPPORTED, "numerator slice exceeds shared memory");
   }

@@ -97,6 +97,13 @@ int64_t workspace_size(int64_t max_states, int64_t total_frames, int64_t precisi
   return int64_t(lfmmi_workspace_size(int32_t(max_states), total_frames, int32_t(precision)));
 }
 
+int64_t chain_loss_workspace_size(int64_t num_h, int64_t den_h, int64_t batch, int64_t max_frames,
+                                  int64_t num_pdfs, int64_t total_frames, int64_t precision) {
+  return int64_t(lfmmi_chain_loss_workspace_size(
+      as_graphs(num_h), as_graphs(den_h), int32_t(batch), int32_t(max_frames), int32_t(num_pdfs),
+      total_frames, int32_t(precision)));
+}
+
 void forward_backward(int64_t h, torch::Tensor row_map, torch::Tensor loglikes,
                       torch::Tensor lengths, double leak, double scale_floor,
                       c10::optional<torch::Tensor> leak_pi, torch::Tensor workspace,
@@ -223,6 +230,7 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("graphs_create", &graphs_create);
   m.def("graphs_destroy", &graphs_destroy);
   m.def("workspace_size", &workspace_size);
+  m.def("chain_loss_workspace_size", &chain_loss_workspace_size);
   m.def("forward_backward", &forward_backward);
   m.def("chain_loss", &chain_loss);
   m.def("forward_kernel", &forward_kernel);

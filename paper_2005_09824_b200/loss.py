@@ -3,9 +3,10 @@
 * :func:`chain_loss` — same signature, result type and failure semantics as
   /root/reference/pkg/src/chainloss/loss.py:42-84 (numpy in, numpy out,
   sorted batch order, ``RuntimeError`` when every utterance fails).  One C-ABI
-  call (``lfmmi_chain_loss``): numerator launch writes gamma_num into the
-  gradient, denominator launch subtracts gamma_den in place, a tiny
-  reduction produces {objective, frames, failed} on device.
+  call (``lfmmi_chain_loss``): the numerator pass (warp per utterance) runs on
+  an auxiliary stream concurrently with the denominator pass (CTA per
+  utterance, writes -gamma_den into the gradient); a combine step adds
+  gamma_num and a tiny reduction produces {objective, frames, failed}.
 * :func:`chain_loss_device` — the same on CUDA tensors, no host sync.
 * :class:`ChainFunction` / :class:`ChainLoss` — the paper's
   ``autograd.Function`` / ``nn.Module``.  With a process group
@@ -61,8 +62,8 @@ def chain_loss_device(values, lengths, numerators, denominator, opts: FBOptions 
     if total_frames is None:
         total_frames = B * T
     prec = 1 if values.dtype == torch.float64 else 0
-    ws = _workspace(dev, ext.workspace_size(max(ng.max_states, dgr.max_states),
-                                            int(total_frames), prec))
+    ws = _workspace(dev, ext.chain_loss_workspace_size(ng.handle, dgr.handle, B, T, D,
+                                                       int(total_frames), prec))
     if grad is None:
         grad = torch.empty_like(values)
     f64 = dict(dtype=torch.float64, device=dev)
