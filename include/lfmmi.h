@@ -86,7 +86,8 @@ size_t lfmmi_workspace_size(int32_t max_states, int64_t total_frames, int32_t pr
  *   loglikes     (B,T,D)    f32/f64 network outputs (log domain)   [device]
  *   lengths      (B)        int32  valid frames per item (>= 1)    [device]
  *   leak_pi      (G,S_max)  f32/f64 custom leak distribution, or NULL for uniform 1/S_g
- *   workspace    device scratch of >= lfmmi_workspace_size(...) bytes
+ *   total_frames an upper bound on sum(lengths) (e.g. B * T_max); sizes the ragged trellis
+ *   workspace    device scratch of >= lfmmi_workspace_size(S_max, total_frames, precision) bytes
  *   posteriors   (B,T,D)    f32/f64  written per `post_mode`; rows of failed items
  *                           are set to zero in every mode; padded rows are zeroed
  *                           by the writing modes (WRITE, NEGATE)
@@ -99,8 +100,9 @@ size_t lfmmi_workspace_size(int32_t max_states, int64_t total_frames, int32_t pr
 int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t *row_map, int32_t batch,
                            int32_t max_frames, int32_t num_pdfs, int32_t precision,
                            const void *loglikes, const int32_t *lengths, double leak,
-                           double scale_floor, const void *leak_pi, void *workspace,
-                           size_t workspace_bytes, void *posteriors, int32_t post_mode,
+                           double scale_floor, const void *leak_pi, int64_t total_frames,
+                           void *workspace, size_t workspace_bytes, void *posteriors,
+                           int32_t post_mode,
                            const int32_t *other_fail, double *log_probs, int32_t *fail_frames,
                            double *scale_logs, void *stream);
 
@@ -125,7 +127,8 @@ int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *num_row_map,
                      int32_t max_frames, int32_t num_pdfs, int32_t precision,
                      const void *loglikes, const int32_t *lengths, double leak,
                      double scale_floor, const void *num_leak_pi, const void *den_leak_pi,
-                     void *workspace, size_t workspace_bytes, void *grad, double *num_log_probs,
+                     int64_t total_frames, void *workspace, size_t workspace_bytes, void *grad,
+                     double *num_log_probs,
                      double *den_log_probs, int32_t *num_fail, int32_t *den_fail,
                      double *totals, void *stream);
 

@@ -289,7 +289,7 @@ extern "C" int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t 
                                       int32_t batch, int32_t max_frames, int32_t num_pdfs,
                                       int32_t precision, const void *loglikes,
                                       const int32_t *lengths, double leak, double scale_floor,
-                                      const void *leak_pi, void *workspace,
+                                      const void *leak_pi, int64_t total_frames, void *workspace,
                                       size_t workspace_bytes, void *posteriors,
                                       int32_t post_mode, const int32_t *other_fail,
                                       double *log_probs, int32_t *fail_frames,
@@ -298,6 +298,10 @@ extern "C" int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t 
   if (rc) return rc;
   if (!row_map || !loglikes || !lengths || !workspace || !posteriors || !log_probs || !fail_frames)
     return set_error(LFMMI_ERR_INVALID, "lfmmi_forward_backward: NULL device pointer");
+  if (total_frames < 1 ||
+      workspace_bytes < lfmmi_workspace_size(graphs->max_states, total_frames, precision))
+    return set_error(LFMMI_ERR_INVALID, "workspace smaller than lfmmi_workspace_size(S_max, "
+                                        "total_frames, precision)");
   if (post_mode < LFMMI_POST_WRITE || post_mode > LFMMI_POST_NEGATE)
     return set_error(LFMMI_ERR_INVALID, "unknown post_mode");
   if (!(leak >= 0.0) || !(scale_floor > 0.0))
@@ -321,8 +325,8 @@ static size_t chain_ws_parts(const lfmmi_graphs *num, const lfmmi_graphs *den, i
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t es = precision == LFMMI_F64 ? 8 : 4;
   const size_t tf = size_t(std::max<int64_t>(total_frames, 1));
-  const size_t den_b = al(size_t(pad4(den ? den->max_states : 1)) * tf * es);
-  const size_t num_b = al(size_t(pad4(num ? num->max_states : 1)) * tf * es);
+  const size_t den_b = al(lfmmi_workspace_size(den ? den->max_states : 1, int64_t(tf), precision));
+  const size_t num_b = al(lfmmi_workspace_size(num ? num->max_states : 1, int64_t(tf), precision));
   const size_t gam_b = al(size_t(batch) * size_t(max_frames) * size_t(num_pdfs) * es);
   if (den_off) *den_off = 0;
   if (num_off) *num_off = den_b;
@@ -380,29 +384,24 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
                                 int32_t batch, int32_t max_frames, int32_t num_pdfs,
                                 int32_t precision, const void *loglikes, const int32_t *lengths,
                                 double leak, double scale_floor, const void *num_leak_pi,
-                                const void *den_leak_pi, void *workspace, size_t workspace_bytes,
-                                void *grad, double *num_log_probs, double *den_log_probs,
+                                const void *den_leak_pi, int64_t total_frames, void *workspace,
+                                size_t workspace_bytes, void *grad, double *num_log_probs,
+                                double *den_log_probs,
                                 int32_t *num_fail, int32_t *den_fail, double *totals,
                                 void *stream) {
   if (!numerators || !denominator)
     return set_error(LFMMI_ERR_INVALID, "lfmmi_chain_loss: NULL graph handle");
-  // Total frames bound the trellis; the caller sized the workspace with
-  // lfmmi_chain_loss_workspace_size for its sum of lengths, which we recover
-  // from the byte count.
   size_t den_off, num_off, gam_off;
-  const size_t es = precision == LFMMI_F64 ? 8 : 4;
-  const size_t gam_b = size_t(batch) * size_t(max_frames) * size_t(num_pdfs) * es;
-  const size_t per_frame =
-      size_t(pad4(denominator->max_states) + pad4(numerators->max_states)) * es;
-  if (workspace_bytes < gam_b + per_frame + 1024)
-    return set_error(LFMMI_ERR_INVALID, "chain_loss workspace too small");
-  const int64_t frames_cap = int64_t((workspace_bytes - gam_b - 1024) / per_frame);
-  chain_ws_parts(numerators, denominator, batch, max_frames, num_pdfs, frames_cap, precision,
-                 &den_off, &num_off, &gam_off);
+  if (total_frames < 1 ||
+      workspace_bytes < chain_ws_parts(numerators, denominator, batch, max_frames, num_pdfs,
+                                       total_frames, precision, &den_off, &num_off, &gam_off))
+    return set_error(LFMMI_ERR_INVALID, "workspace smaller than lfmmi_chain_loss_workspace_size");
   char *ws = static_cast<char *>(workspace);
   const size_t num_bytes = gam_off - num_off, den_bytes = num_off - den_off;
   auto st = static_cast<cudaStream_t>(stream);
   AuxStream &ax = aux_for_device();
+  const bool serial = std::getenv("LFMMI_SERIAL_CHAIN") != nullptr;
+  cudaStream_t nst = serial ? st : ax.aux;
   // Fork: the numerator pass (small graphs, latency-bound, one warp per
   // utterance) runs on the auxiliary stream next to the denominator pass (one
   // CTA per utterance).  The denominator is launched first so its CTAs claim
@@ -410,18 +409,18 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
   int rc = check_cuda(cudaEventRecord(ax.fork, st), "cudaEventRecord(fork)");
   if (rc) return rc;
   rc = lfmmi_forward_backward(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
-                              loglikes, lengths, leak, scale_floor, den_leak_pi, ws + den_off,
-                              den_bytes, grad, LFMMI_POST_NEGATE, nullptr, den_log_probs,
+                              loglikes, lengths, leak, scale_floor, den_leak_pi, total_frames,
+                              ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE, nullptr, den_log_probs,
                               den_fail, nullptr, stream);
   if (rc) return rc;
   rc = check_cuda(cudaStreamWaitEvent(ax.aux, ax.fork, 0), "cudaStreamWaitEvent(fork)");
   if (rc) return rc;
   rc = lfmmi_forward_backward(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
-                              loglikes, lengths, leak, scale_floor, num_leak_pi, ws + num_off,
-                              num_bytes, ws + gam_off, LFMMI_POST_WRITE, nullptr, num_log_probs,
-                              num_fail, nullptr, ax.aux);
+                              loglikes, lengths, leak, scale_floor, num_leak_pi, total_frames,
+                              ws + num_off, num_bytes, ws + gam_off, LFMMI_POST_WRITE, nullptr, num_log_probs,
+                              num_fail, nullptr, nst);
   if (rc) return rc;
-  rc = check_cuda(cudaEventRecord(ax.join, ax.aux), "cudaEventRecord(join)");
+  rc = check_cuda(cudaEventRecord(ax.join, nst), "cudaEventRecord(join)");
   if (rc) return rc;
   rc = check_cuda(cudaStreamWaitEvent(st, ax.join, 0), "cudaStreamWaitEvent(join)");
   if (rc) return rc;

@@ -106,7 +106,8 @@ int64_t chain_loss_workspace_size(int64_t num_h, int64_t den_h, int64_t batch, i
 
 void forward_backward(int64_t h, torch::Tensor row_map, torch::Tensor loglikes,
                       torch::Tensor lengths, double leak, double scale_floor,
-                      c10::optional<torch::Tensor> leak_pi, torch::Tensor workspace,
+                      c10::optional<torch::Tensor> leak_pi, int64_t total_frames,
+                      torch::Tensor workspace,
                       torch::Tensor posteriors, int64_t post_mode,
                       c10::optional<torch::Tensor> other_fail, torch::Tensor log_probs,
                       torch::Tensor fail_frames, c10::optional<torch::Tensor> scale_logs) {
@@ -125,7 +126,7 @@ void forward_backward(int64_t h, torch::Tensor row_map, torch::Tensor loglikes,
                                int32_t(loglikes.size(1)), int32_t(loglikes.size(2)),
                                precision_of(loglikes), loglikes.data_ptr(),
                                lengths.data_ptr<int32_t>(), leak, scale_floor,
-                               ptr_or_null<void>(leak_pi), workspace.data_ptr(),
+                               ptr_or_null<void>(leak_pi), total_frames, workspace.data_ptr(),
                                size_t(workspace.numel()), posteriors.data_ptr(), int32_t(post_mode),
                                ptr_or_null<int32_t>(other_fail), log_probs.data_ptr<double>(),
                                fail_frames.data_ptr<int32_t>(), ptr_or_null<double>(scale_logs),
@@ -136,7 +137,7 @@ void forward_backward(int64_t h, torch::Tensor row_map, torch::Tensor loglikes,
 void chain_loss(int64_t num_h, torch::Tensor num_row_map, int64_t den_h, torch::Tensor den_row_map,
                 torch::Tensor loglikes, torch::Tensor lengths, double leak, double scale_floor,
                 c10::optional<torch::Tensor> num_leak_pi, c10::optional<torch::Tensor> den_leak_pi,
-                torch::Tensor workspace, torch::Tensor grad, torch::Tensor num_log_probs,
+                int64_t total_frames, torch::Tensor workspace, torch::Tensor grad, torch::Tensor num_log_probs,
                 torch::Tensor den_log_probs, torch::Tensor num_fail, torch::Tensor den_fail,
                 torch::Tensor totals) {
   const c10::cuda::CUDAGuard guard(loglikes.device());
@@ -158,7 +159,7 @@ void chain_loss(int64_t num_h, torch::Tensor num_row_map, int64_t den_h, torch::
                          int32_t(loglikes.size(1)), int32_t(loglikes.size(2)),
                          precision_of(loglikes), loglikes.data_ptr(), lengths.data_ptr<int32_t>(),
                          leak, scale_floor, ptr_or_null<void>(num_leak_pi),
-                         ptr_or_null<void>(den_leak_pi), workspace.data_ptr(),
+                         ptr_or_null<void>(den_leak_pi), total_frames, workspace.data_ptr(),
                          size_t(workspace.numel()), grad.data_ptr(),
                          num_log_probs.data_ptr<double>(), den_log_probs.data_ptr<double>(),
                          num_fail.data_ptr<int32_t>(), den_fail.data_ptr<int32_t>(),

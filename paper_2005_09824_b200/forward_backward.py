@@ -189,8 +189,8 @@ def forward_backward_device(values, lengths, graphs, opts: FBOptions = FBOptions
     fail = torch.empty(B, dtype=torch.int32, device=dev)
     sl = torch.empty((B, T), dtype=torch.float64, device=dev) if want_scale_logs else None
     ext.forward_backward(dg.handle, dg.row_map, values, lengths, float(opts.leak_coefficient),
-                         float(opts.scale_floor), pi_t, ws, posteriors, int(mode), other_fail,
-                         logp, fail, sl)
+                         float(opts.scale_floor), pi_t, int(total_frames), ws, posteriors,
+                         int(mode), other_fail, logp, fail, sl)
     return posteriors, logp, fail, sl
 
 

@@ -72,7 +72,8 @@ def chain_loss_device(values, lengths, numerators, denominator, opts: FBOptions 
     num_fail, den_fail = torch.empty(B, **i32), torch.empty(B, **i32)
     totals = torch.empty(3, **f64)
     ext.chain_loss(ng.handle, ng.row_map, dgr.handle, dgr.row_map, values, lengths,
-                   float(opts.leak_coefficient), float(opts.scale_floor), pn, pd, ws, grad,
+                   float(opts.leak_coefficient), float(opts.scale_floor), pn, pd,
+                   int(total_frames), ws, grad,
                    num_lp, den_lp, num_fail, den_fail, totals)
     return grad, num_lp, den_lp, num_fail, den_fail, totals
 

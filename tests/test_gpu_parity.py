@@ -251,3 +251,35 @@ def test_pdf_mismatch_raises(cuda):
     batch = P.make_batch([np.zeros((2, 2))])
     with pytest.raises(ValueError, match="pdf dimension"):
         P.chain_loss(batch, P.ChainGraphBatch.broadcast(loop, 1), P.ChainGraphBatch.broadcast(loop, 1))
+
+
+def test_chain_loss_exact_workspace_concurrent_repeat(cuda):
+    """Regression: numerator and denominator passes run concurrently and share one
+    exactly-sized workspace; repeated calls must not overlap their regions."""
+    import torch
+
+    from paper_2005_09824_b200 import _backend
+
+    ext = _backend.ext()
+    w = synth.make_workload("wsj_mono", seed=3, batch_size=8)
+    batch, nums, den = w.build(P)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    dev = torch.device("cuda", 0)
+    values = torch.tensor(batch.values, dtype=torch.float32, device=dev)
+    lengths = torch.tensor(batch.lengths, dtype=torch.int32, device=dev)
+    ng, dg = P.device_graphs(nums, dev), P.device_graphs(den, dev)
+    B, T, D = values.shape
+    tf = int(batch.lengths.sum())
+    ws = torch.empty(ext.chain_loss_workspace_size(ng.handle, dg.handle, B, T, D, tf, 0),
+                     dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        grad = torch.empty_like(values)
+        f64, i32 = dict(dtype=torch.float64, device=dev), dict(dtype=torch.int32, device=dev)
+        nl, dl, tot = torch.empty(B, **f64), torch.empty(B, **f64), torch.empty(3, **f64)
+        nf, df = torch.empty(B, **i32), torch.empty(B, **i32)
+        ext.chain_loss(ng.handle, ng.row_map, dg.handle, dg.row_map, values, lengths, 1e-5,
+                       1e-300, None, None, tf, ws, grad, nl, dl, nf, df, tot)
+        assert np.abs(grad.double().cpu().numpy() - ref.grad).max() <= FP32_GRAD_ABS
+    with pytest.raises(ValueError, match="workspace"):
+        ext.chain_loss(ng.handle, ng.row_map, dg.handle, dg.row_map, values, lengths, 1e-5,
+                       1e-300, None, None, tf, ws[:-1024], grad, nl, dl, nf, df, tot)
