@@ -379,7 +379,7 @@ def run_ours(args):
                          "peak_source": peak_src},
             "kernel_ms": {"den_fused": kt["den"], "num_fused": kt["num"],
                           "den_share_of_step": kt["den"] / ms_per_step},
-            "e2e": e2e, "gpu_launches": 3 * args.steps, "cpu_baseline": cpu, "clocks": clocks,
+            "e2e": e2e, "gpu_launches": 4 * args.steps, "cpu_baseline": cpu, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if pg is not None:
