@@ -374,7 +374,7 @@ def run_ours(args):
                        "parallelism": f"dp{world} (sequence-sharded, scalar all-reduce)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "fb_tile_kernel<float,1024> (denominator pass)",
+                         "kernel": "fb_tile_kernel<float,512> (denominator pass)",
                          "algorithmic_bytes_per_launch": A, "launch_ms": kt["den"],
                          "peak_source": peak_src},
             "kernel_ms": {"den_fused": kt["den"], "num_fused": kt["num"],

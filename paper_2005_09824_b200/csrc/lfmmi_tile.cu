@@ -1,10 +1,10 @@
 // Tile kernels: the LF-MMI hot path for both graph classes.
 //
-//   fb_tile_kernel<Real, 1024, 1, true>  — denominator: one 1024-thread CTA
+//   fb_tile_kernel<Real, 512, 1, true, .>  — denominator: one 512-thread CTA
 //       per utterance; the arc layout of the current phase is resident in
 //       shared memory (CSR-by-destination for the forward, CSR-by-source for
 //       the backward).
-//   fb_tile_kernel<Real, 32, IPC, false> — numerators: one warp per
+//   fb_tile_kernel<Real, 32, IPC, ., .> — numerators: one warp per
 //       utterance (IPC utterances per CTA, __syncwarp only); the tiny
 //       per-utterance arc packs are read through L1.
 //
@@ -102,9 +102,10 @@ __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int
 
 template <int BLOCK>
 __device__ __forceinline__ void copy16(void *dst, const void *src, size_t bytes, int tid) {
-  const char *s = static_cast<const char *>(src);
-  char *d = static_cast<char *>(dst);
-  for (size_t c = size_t(tid) * 16; c < bytes; c += size_t(BLOCK) * 16) cp_async_16(d + c, s + c);
+  const int4 *s = static_cast<const int4 *>(src);
+  int4 *d = static_cast<int4 *>(dst);
+  const int n = int(bytes >> 4);
+  for (int c = tid; c < n; c += BLOCK) cp_async_16(d + c, s + c);
 }
 
 template <int GROUP, int IPC>
@@ -151,7 +152,7 @@ struct SlotOf<float> { using type = SlotF32; };
 template <>
 struct SlotOf<double> { using type = SlotF64; };
 
-template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH>
+template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI>
 __global__ void __launch_bounds__(GROUP *IPC, 1)
     fb_tile_kernel(const FBArgs<Real> a, int Fmax, int ntiles_max, int X_pad) {
   constexpr int NW = GROUP / 32;
@@ -159,6 +160,11 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   extern __shared__ __align__(16) unsigned char smem_all[];
   const int gid = threadIdx.x / GROUP;
   const int tid = threadIdx.x % GROUP, lane = tid & 31, warp = tid >> 5;
+  // Per-frame chores (emission rows, prefetch, posterior flush) run on the
+  // *last* warps, which the snake tile order gives the lightest arc tiles.
+  const int ctid = GROUP - 1 - tid, cwarp = ctid >> 5;
+  const int ntile_rounds_max = (ntiles_max + NW - 1) / NW;
+  (void)ntile_rounds_max;
   const int b = blockIdx.x * IPC + gid;
   if (b >= a.B) return;  // whole group exits together (no CTA-wide barriers for IPC > 1)
   const TileLayout lay = tile_layout(SMEM_GRAPH, Fmax, ntiles_max, a.D, X_pad, a.S_pad, a.D_pad,
@@ -193,7 +199,11 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   const int mode = a.mode;
   const bool reads_post = mode == kPostAdd || mode == kPostSubtract;
   const bool other_failed = a.other_fail != nullptr && a.other_fail[b] >= 0;
-  const int nrw = (D + 31) / 32 < NW ? (D + 31) / 32 : NW;  // warps holding row elements
+  const int nrw = (D + 31) / 32 < NW ? (D + 31) / 32 : NW;  // chore warps holding row elements
+  const int nrounds = (ntiles + NW - 1) / NW;
+  // Snake order: round r gives warp w tile r*NW + w (r even) or r*NW + NW-1-w
+  // (r odd), pairing heavy and light tiles (tiles are sorted by degree).
+  auto tile_of = [&](int r) { return r * NW + ((r & 1) ? NW - 1 - warp : warp); };
 
   // Arc-pack views of the current phase: shared memory (denominator) or L1 (numerators).
   const unsigned *tinfo;
@@ -252,7 +262,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   long long off = 0;
   for (int j = tid; j < b; j += GROUP) off += a.lengths[j];
   off = warp_sum(off);
-  const Real *pi = a.leak_pi ? a.leak_pi + size_t(row) * a.S_max : nullptr;
+  const Real *pi = CUSTOM_PI ? a.leak_pi + size_t(row) * a.S_max : nullptr;
   double psum_d = 0.0;
   if (pi)
     for (int s = tid; s < S; s += GROUP) psum_d += double(pi[s]);
@@ -279,20 +289,21 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   }
 
   auto issue_row = [&](int t) {
-    if (t < 0 || t >= T) return;
+    if (t < 0 || t >= T || cwarp >= nrw) return;
     const Real *src = Lb + size_t(t) * D;
     Real *dst = stage + (t & 3) * D_pad;
-    for (int d = tid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
+    for (int d = ctid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
   };
   auto row_max_part = [&](int t) {
-    if (t < 0 || t >= T || warp >= nrw) return;
+    if (t < 0 || t >= T || cwarp >= nrw) return;
     const Real *src = stage + (t & 3) * D_pad;
     Real m = -INFINITY;
-    for (int d = tid; d < D; d += GROUP) m = fmax(m, src[d]);
+    for (int d = ctid; d < D; d += GROUP) m = fmax(m, src[d]);
     m = warp_max(m);
-    if (lane == 0) mpart[(t & 1) * 32 + warp] = m;
+    if (lane == 0) mpart[(t & 1) * 32 + cwarp] = m;
   };
   auto compute_e = [&](int t, bool record_shift) {
+    if (cwarp >= nrw) return;
     const Real *mp = mpart + (t & 1) * 32;
     Real m;
     if constexpr (NW == 1) {
@@ -303,8 +314,8 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     }
     const Real *src = stage + (t & 3) * D_pad;
     Real *dst = ebuf + (t & 1) * D_pad;
-    for (int d = tid; d < D; d += GROUP) dst[d] = exp_r(src[d] - m);
-    if (record_shift && tid == 0) shifts[t] = m;
+    for (int d = ctid; d < D; d += GROUP) dst[d] = exp_r(src[d] - m);
+    if (record_shift && ctid == 0) shifts[t] = m;
   };
 
   // ---- prologue -----------------------------------------------------------------
@@ -342,7 +353,12 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     {
       const Real *r = rbuf + cur * S_pad;
       Real *arow = trellis + size_t(k) * S_pad;
-      for (int s = tid; s < S; s += GROUP) arow[s] = (r[s] + leakc * (pi ? pi[s] : upi)) * inv2;
+      if constexpr (CUSTOM_PI) {
+        for (int s = tid; s < S; s += GROUP) arow[s] = (r[s] + leakc * pi[s]) * inv2;
+      } else {
+        const Real lu = leakc * upi;
+        for (int s = tid; s < S; s += GROUP) arow[s] = (r[s] + lu) * inv2;
+      }
     }
     if (k + 1 < T) compute_e(k + 1, true);
     issue_row(k + 2);
@@ -353,7 +369,9 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       Real *rn = rbuf + nxt * S_pad;
       const bool last = (k + 1 == T);
       Real psum = Real(0);
-      for (int tile = warp; tile < ntiles; tile += NW) {
+      for (int rr = 0; rr < nrounds; ++rr) {
+        const int tile = tile_of(rr);
+        if (tile >= ntiles) continue;
         const unsigned info = tinfo[tile * 32 + lane];
         const int trips = ttrips[tile];
         const int base = tbase[tile] + lane;
@@ -367,7 +385,10 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
             const Real w = p * e[wd >> 16];
             const int src = int(wd & 0xFFFFu);
             A = fma(w, r[src], A);
-            Bs = pi ? fma(w, pi[src], Bs) : Bs + w;
+            if constexpr (CUSTOM_PI)
+              Bs = fma(w, pi[src], Bs);
+            else
+              Bs += w;
           }
         } else {
 #pragma unroll 4
@@ -380,7 +401,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
         }
         const int s = int(info & 0xFFFFu);
         if (s != 0xFFFF) {
-          Real raw = inv2 * (A + leakc * (pi ? Bs : upi * Bs));
+          Real raw = inv2 * (A + leakc * (CUSTOM_PI ? Bs : upi * Bs));
           if (last) raw *= fin[s];
           rn[s] = raw;
           psum += raw;
@@ -450,19 +471,19 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   auto issue_alpha = [&](int k) {
     if (k < 0) return;
     copy16<GROUP>(aring + (k & 1) * S_pad, trellis + size_t(k) * S_pad,
-                  size_t(S_pad) * sizeof(Real), tid);
+                  size_t(S_pad) * sizeof(Real), ctid);
   };
   auto issue_post = [&](int t) {
     if (!reads_post || t < 0 || t >= T) return;
     const Real *src = post_b + size_t(t) * D;
     Real *dst = gstage + (t & 1) * D_pad;
-    for (int d = tid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
+    for (int d = ctid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
   };
   // gamma_t[d] = sum of pdf d's slots (float4 loads, 4 accumulators).
   auto flush_post = [&](int t, const Real *xt) {
     Real *prow = post_b + size_t(t) * D;
     const Real *old = gstage + (t & 1) * D_pad;
-    for (int d = tid; d < D; d += GROUP) {
+    for (int d = ctid; d < D; d += GROUP) {
       const Real g = sum_groups4(xt + pdfptr[d], (pdfptr[d + 1] - pdfptr[d]) >> 2);
       switch (mode) {
         case kPostNegate: prow[d] = -g; break;
@@ -503,7 +524,9 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       Real *bn = rbuf + cp * S_pad;
       Real *xt = xterm + cp * X_pad;
       Real dp = Real(0);
-      for (int tile = warp; tile < ntiles; tile += NW) {
+      for (int rr = 0; rr < nrounds; ++rr) {
+        const int tile = tile_of(rr);
+        if (tile >= ntiles) continue;
         const unsigned info = tinfo[tile * 32 + lane];
         const int trips = ttrips[tile];
         const int base = tbase[tile] + lane;
@@ -522,7 +545,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
         if (s != 0xFFFF) {
           const Real v = inv * A;
           bn[s] = v;
-          dp = fma(pi ? pi[s] : upi, v, dp);
+          dp = fma(CUSTOM_PI ? pi[s] : upi, v, dp);
         }
       }
       dp = warp_sum(dp);
@@ -535,23 +558,34 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   flush_post(0, xterm);
 }
 
-template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH>
-static int launch_tile_impl(const FBArgs<Real> &a, const lfmmi_graphs *g, size_t per_item,
-                            cudaStream_t st) {
+template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI>
+static int launch_tile_impl2(const FBArgs<Real> &a, const lfmmi_graphs *g, size_t per_item,
+                             cudaStream_t st) {
   static bool configured = false;
+  auto kern = fb_tile_kernel<Real, GROUP, IPC, SMEM_GRAPH, CUSTOM_PI>;
   if (!configured) {
-    int rc = check_cuda(cudaFuncSetAttribute(fb_tile_kernel<Real, GROUP, IPC, SMEM_GRAPH>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
-                        "cudaFuncSetAttribute(tile)");
+    int rc = check_cuda(
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
+        "cudaFuncSetAttribute(tile)");
     if (rc) return rc;
     configured = true;
   }
   const int grid = (a.B + IPC - 1) / IPC;
   const int Fmax = std::max(g->max_tf_slots, g->max_tb_slots);
-  fb_tile_kernel<Real, GROUP, IPC, SMEM_GRAPH><<<grid, GROUP * IPC, per_item * IPC, st>>>(
-      a, Fmax, g->max_tiles, pad4(std::max(4, g->max_xpad)));
+  kern<<<grid, GROUP * IPC, per_item * IPC, st>>>(a, Fmax, g->max_tiles,
+                                                  pad4(std::max(4, g->max_xpad)));
   return check_cuda(cudaGetLastError(), "fb_tile_kernel launch");
 }
+
+template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH>
+static int launch_tile_impl(const FBArgs<Real> &a, const lfmmi_graphs *g, size_t per_item,
+                            cudaStream_t st) {
+  if (a.leak_pi) return launch_tile_impl2<Real, GROUP, IPC, SMEM_GRAPH, true>(a, g, per_item, st);
+  return launch_tile_impl2<Real, GROUP, IPC, SMEM_GRAPH, false>(a, g, per_item, st);
+}
+
+// Threads per utterance for the shared-memory (denominator) tile kernel.
+constexpr int kDenGroup = 512;
 
 template <typename Real>
 int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item,
@@ -576,11 +610,11 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     return set_error(LFMMI_ERR_UNSUPPORTED, "numerator slice exceeds shared memory");
   }
   const size_t per = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
-                                 a.T_pad, 32, real).total;
+                                 a.T_pad, kDenGroup / 32, real).total;
   if (per > size_t(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "tile pack needs " + std::to_string(per) + " B shared memory");
-  return launch_tile_impl<Real, 1024, 1, true>(a, g, per, st);
+  return launch_tile_impl<Real, kDenGroup, 1, true>(a, g, per, st);
 }
 
 template int launch_tile<float>(const FBArgs<float> &, const lfmmi_graphs *, bool, cudaStream_t);
