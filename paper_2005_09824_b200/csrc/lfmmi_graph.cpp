@@ -265,7 +265,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
     max_chunks = std::max(max_chunks, nchunks);
 
     // ---- tile packs (16-bit state / pdf / posterior-slot encoding) ----
-    bool tileable = S <= 65535 && num_pdfs <= 65535 && I <= 65535 && mi < 65536 && mo < 65536;
+    bool tileable = S <= 16383 && num_pdfs <= 16383 && I <= 65535 && mi < 65536 && mo < 65536;
     d[kTileOff] = int(h.tf_trips.size());
     d[kTfSlotOff] = int(h.tf_word.size());
     d[kTbSlotOff] = int(h.tb_word.size());
@@ -335,17 +335,22 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
       }
       for (int a : tb.arc_of_slot)
         h.tb_xslot.push_back((unsigned short)(a < 0 ? dummy_slot : xslot_of_arc[a]));
+      // fp32 slots carry byte offsets (index * 4) so the gather addresses are
+      // one shift-add each; requires S, D <= 16383 (checked by kTileable).
+      auto bytes_word = [](unsigned w) {
+        return ((w & 0xFFFFu) << 2) | (((w >> 16) << 2) << 16);
+      };
       for (size_t k = 0; k < tf.word.size(); ++k) {
         float f = float(tf.prob[k]);
         unsigned bits;
         std::memcpy(&bits, &f, 4);
-        h.tf_wp.push_back({tf.word[k], bits});
+        h.tf_wp.push_back({bytes_word(tf.word[k]), bits});
       }
       for (size_t k = 0; k < tb.word.size(); ++k) {
         float f = float(tb.prob[k]);
         unsigned bits;
         std::memcpy(&bits, &f, 4);
-        h.tb_wp.push_back({tb.word[k], bits});
+        h.tb_wp.push_back({bytes_word(tb.word[k]), bits});
       }
       max_xpad = std::max(max_xpad, xpad);
       d[kTfSlots] = int(tf.word.size());

@@ -33,6 +33,7 @@
 #include "lfmmi_kernels.h"
 
 #include <string>
+#include <type_traits>
 
 namespace lfmmi {
 
@@ -133,7 +134,7 @@ struct SlotF32 {
   const uint2 *wp;
   __device__ __forceinline__ void load(int slot, unsigned &w, float &p) const {
     const uint2 v = wp[slot];
-    w = v.x;
+    w = ((v.x & 0xFFFFu) >> 2) | ((v.x >> 18) << 16);  // byte offsets -> indices
     p = __uint_as_float(v.y);
   }
 };
@@ -151,6 +152,91 @@ template <>
 struct SlotOf<float> { using type = SlotF32; };
 template <>
 struct SlotOf<double> { using type = SlotF64; };
+
+// ---- 32-bit shared-space accessors (explicitly scheduled fp32 inner loops) ----
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_f(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_h(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(a), "f"(v));
+}
+
+// Forward arc sums of one tile lane, fp32 (slots hold byte-offset words):
+// A = sum p e[pdf] r[src], Bs = sum p e[pdf] (leak mass, uniform pi).
+template <bool LEAKY>
+__device__ __forceinline__ void fwd_tile_f32(uint32_t sb, int trips, uint32_t e32, uint32_t r32,
+                                             float &A, float &Bs) {
+  int j = 0;
+  for (; j + 4 <= trips; j += 4, sb += 4 * 256) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
+                w3 = lds_v2(sb + 768);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
+                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
+    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu)),
+                r2 = lds_f(r32 + (w2.x & 0xFFFFu)), r3 = lds_f(r32 + (w3.x & 0xFFFFu));
+    const float q0 = __uint_as_float(w0.y) * e0, q1 = __uint_as_float(w1.y) * e1,
+                q2 = __uint_as_float(w2.y) * e2, q3 = __uint_as_float(w3.y) * e3;
+    A = fmaf(q0, r0, A);
+    A = fmaf(q1, r1, A);
+    A = fmaf(q2, r2, A);
+    A = fmaf(q3, r3, A);
+    if (LEAKY) Bs += (q0 + q1) + (q2 + q3);
+  }
+  for (; j < trips; ++j, sb += 256) {
+    const uint2 w = lds_v2(sb);
+    const float q = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16));
+    A = fmaf(q, lds_f(r32 + (w.x & 0xFFFFu)), A);
+    if (LEAKY) Bs += q;
+  }
+}
+
+// Backward arc sums of one tile lane, fp32: term = p e[pdf] (b[dst] + ld);
+// A = sum term, posterior slot xs <- as * term.
+__device__ __forceinline__ float bwd_tile_f32(uint32_t sb, uint32_t xb, int trips, uint32_t e32,
+                                              uint32_t b32, uint32_t x32, float ld, float as) {
+  float A = 0.f;
+  int j = 0;
+  for (; j + 4 <= trips; j += 4, sb += 4 * 256, xb += 4 * 64) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
+                w3 = lds_v2(sb + 768);
+    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64), x2 = lds_h(xb + 128),
+                   x3 = lds_h(xb + 192);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
+                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
+    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu)),
+                b2 = lds_f(b32 + (w2.x & 0xFFFFu)), b3 = lds_f(b32 + (w3.x & 0xFFFFu));
+    const float t0 = __uint_as_float(w0.y) * e0 * (b0 + ld),
+                t1 = __uint_as_float(w1.y) * e1 * (b1 + ld),
+                t2 = __uint_as_float(w2.y) * e2 * (b2 + ld),
+                t3 = __uint_as_float(w3.y) * e3 * (b3 + ld);
+    A += (t0 + t1) + (t2 + t3);
+    sts_f(x32 + 4 * x0, as * t0);
+    sts_f(x32 + 4 * x1, as * t1);
+    sts_f(x32 + 4 * x2, as * t2);
+    sts_f(x32 + 4 * x3, as * t3);
+  }
+  for (; j < trips; ++j, sb += 256, xb += 64) {
+    const uint2 w = lds_v2(sb);
+    const uint32_t x = lds_h(xb);
+    const float t = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16)) *
+                    (lds_f(b32 + (w.x & 0xFFFFu)) + ld);
+    A += t;
+    sts_f(x32 + 4 * x, as * t);
+  }
+  return A;
+}
 
 template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI>
 __global__ void __launch_bounds__(GROUP *IPC, 1)
@@ -184,6 +270,11 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   Real *part = reinterpret_cast<Real *>(smem + lay.part);
   Real *mpart = reinterpret_cast<Real *>(smem + lay.mpart);
   auto gsync = [] { tsync<GROUP, IPC>(); };
+  // fp32 + shared-memory arc pack: explicitly scheduled loops on byte-offset words.
+  constexpr bool FAST = std::is_same<Real, float>::value && SMEM_GRAPH && !CUSTOM_PI;
+  const uint32_t wp32 = smem_u32(smem + lay.wp), xs32 = smem_u32(smem + lay.xs);
+  (void)wp32;
+  (void)xs32;
 
   const int T = a.lengths[b];
   const int D = a.D;
@@ -368,6 +459,9 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       const Real *r = rbuf + cur * S_pad;
       Real *rn = rbuf + nxt * S_pad;
       const bool last = (k + 1 == T);
+      const uint32_t e32 = smem_u32(e), r32 = smem_u32(r);
+      (void)e32;
+      (void)r32;
       Real psum = Real(0);
       for (int rr = 0; rr < nrounds; ++rr) {
         const int tile = tile_of(rr);
@@ -376,7 +470,13 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
         const int trips = ttrips[tile];
         const int base = tbase[tile] + lane;
         Real A = Real(0), Bs = Real(0);
-        if (leakc != Real(0)) {
+        if constexpr (FAST) {
+          const uint32_t sb = wp32 + uint32_t(base) * 8u;
+          if (leakc != Real(0))
+            fwd_tile_f32<true>(sb, trips, e32, r32, A, Bs);
+          else
+            fwd_tile_f32<false>(sb, trips, e32, r32, A, Bs);
+        } else if (leakc != Real(0)) {
 #pragma unroll 4
           for (int j = 0; j < trips; ++j) {
             unsigned wd;
@@ -533,14 +633,19 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
         const int s = int(info & 0xFFFFu);
         const Real as = (s != 0xFFFF) ? al[s] * inv : Real(0);
         Real A = Real(0);
+        if constexpr (FAST) {
+          A = bwd_tile_f32(wp32 + uint32_t(base) * 8u, xs32 + uint32_t(base) * 2u, trips,
+                           smem_u32(e), smem_u32(bt), smem_u32(xt), ld, as);
+        } else {
 #pragma unroll 4
-        for (int j = 0; j < trips; ++j) {
-          unsigned wd;
-          Real p;
-          slot.load(base + 32 * j, wd, p);
-          const Real term = p * e[wd >> 16] * (bt[wd & 0xFFFFu] + ld);
-          A += term;
-          xt[XS[base + 32 * j]] = as * term;
+          for (int j = 0; j < trips; ++j) {
+            unsigned wd;
+            Real p;
+            slot.load(base + 32 * j, wd, p);
+            const Real term = p * e[wd >> 16] * (bt[wd & 0xFFFFu] + ld);
+            A += term;
+            xt[XS[base + 32 * j]] = as * term;
+          }
         }
         if (s != 0xFFFF) {
           const Real v = inv * A;
