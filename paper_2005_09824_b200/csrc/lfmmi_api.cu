@@ -247,6 +247,17 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
   a.fail = fail;
   a.scale_logs = scale_logs;
   a.I_pad = pad4(std::max(1, graphs->max_arcs));
+  if (std::is_same<Real, float>::value) {  // f32 tile slots address replicated vectors
+    a.rep_r = graphs->rep_r;
+    a.r_stride = graphs->r_stride;
+    a.rep_e = graphs->rep_e;
+    a.e_stride = graphs->e_stride;
+  } else {  // f64 tile slots use plain indices
+    a.rep_r = 1;
+    a.r_stride = a.S_pad;
+    a.rep_e = 1;
+    a.e_stride = a.D_pad;
+  }
   if (work_bytes < size_t(a.S_pad) * sizeof(Real))
     return set_error(LFMMI_ERR_INVALID, "workspace too small");
   // Numerator-sized graphs: one warp per utterance.  Larger graphs: one CTA

@@ -77,6 +77,7 @@ struct FBArgs {
   int *fail;
   double *scale_logs;
   int I_pad;  // tile kernel: per-arc scratch (posterior slots)
+  int rep_r, r_stride, rep_e, e_stride;  // tile kernel: gather-vector replication
 };
 
 }  // namespace lfmmi

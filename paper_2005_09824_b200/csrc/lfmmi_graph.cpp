@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "lfmmi_internal.h"
+#include "lfmmi_schedule.h"
 
 namespace lfmmi {
 
@@ -67,56 +68,6 @@ struct HostPack {
   std::vector<uint2> tf_wp, tb_wp;
 };
 
-// Tile pack of one CSR layout: states sorted by degree (descending, stable)
-// into 32-lane tiles; tile w holds 32 * trips_w slots, slot j of lane l at
-// base_w + 32 j + l.  Padded slots carry probability 0 and index 0.
-struct TilePack {
-  std::vector<unsigned> info, word;
-  std::vector<int> trips, base;
-  std::vector<double> prob;
-  std::vector<int> arc_of_slot;  // CSR arc index per slot (-1 = padding)
-};
-
-TilePack make_tiles(int S, const std::vector<int> &ptr, const std::vector<unsigned> &arc_word,
-                    const std::vector<double> &arc_prob) {
-  TilePack tp;
-  std::vector<int> order(S);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-    return (ptr[x + 1] - ptr[x]) > (ptr[y + 1] - ptr[y]);
-  });
-  const int ntiles = (S + 31) / 32;
-  int base = 0;
-  for (int w = 0; w < ntiles; ++w) {
-    const int s0 = order[32 * w];
-    const int trips = ptr[s0 + 1] - ptr[s0];
-    tp.trips.push_back(trips);
-    tp.base.push_back(base);
-    const size_t start = tp.word.size();
-    tp.word.resize(start + size_t(32) * trips, 0u);
-    tp.prob.resize(start + size_t(32) * trips, 0.0);
-    tp.arc_of_slot.resize(start + size_t(32) * trips, -1);
-    for (int l = 0; l < 32; ++l) {
-      const int k = 32 * w + l;
-      if (k >= S) {
-        tp.info.push_back(0xFFFFu);
-        continue;
-      }
-      const int s = order[k];
-      const int deg = ptr[s + 1] - ptr[s];
-      tp.info.push_back(unsigned(s) | (unsigned(deg) << 16));
-      for (int j = 0; j < deg; ++j) {
-        const size_t slot = start + size_t(32) * j + l;
-        tp.word[slot] = arc_word[ptr[s] + j];
-        tp.prob[slot] = arc_prob[ptr[s] + j];
-        tp.arc_of_slot[slot] = ptr[s] + j;
-      }
-    }
-    base += 32 * trips;
-  }
-  return tp;
-}
-
 // Chunk length for the pdf-grouped posterior gather: aim for about one chunk
 // per thread of the largest block (1024), never longer than needed.
 int chunk_len_for(int num_arcs) { return std::max(2, (num_arcs + 1023) / 1024); }
@@ -148,6 +99,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
 
   HostPack h;
   h.desc.resize(size_t(num_rows) * kDescInts, 0);
+  const GatherLayout gl = make_gather_layout(max_states, num_pdfs);
   int max_chunks = 0, max_in = 0, max_out = 0;
   int max_tiles = 0, max_tf = 0, max_tb = 0, max_xpad = 0;
   bool all_tileable = true;
@@ -264,102 +216,76 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
     d[kNumChunks] = nchunks;
     max_chunks = std::max(max_chunks, nchunks);
 
-    // ---- tile packs (16-bit state / pdf / posterior-slot encoding) ----
+    // ---- tile packs (scheduled, 16-bit state / pdf / posterior-slot encoding) ----
     bool tileable = S <= 16383 && num_pdfs <= 16383 && I <= 65535 && mi < 65536 && mo < 65536;
     d[kTileOff] = int(h.tf_trips.size());
     d[kTfSlotOff] = int(h.tf_word.size());
     d[kTbSlotOff] = int(h.tb_word.size());
     d[kPdfPtrOff2] = int(h.pdf_arc_ptr.size());
-    // Posterior slot of every forward_* arc: grouped by pdf (forward_* order
-    // inside a group), each group padded to a multiple of 4 slots so the
-    // per-pdf sum reads whole float4s; one trailing dummy slot absorbs the
-    // writes of padded tile slots.
-    std::vector<int> xslot_of_arc(I);
-    int xpad = 0;
-    {
-      std::vector<int> cnt(num_pdfs, 0);
-      for (int a = 0; a < I; ++a) cnt[fw_pdf[base + a]]++;
-      std::vector<int> start(num_pdfs + 1, 0);
-      for (int p = 0; p < num_pdfs; ++p) start[p + 1] = start[p] + ((cnt[p] + 3) & ~3);
-      for (int p = 0; p <= num_pdfs; ++p) h.pdf_arc_ptr.push_back(start[p]);
-      std::vector<int> fill(start.begin(), start.end() - 1);
-      for (int a = 0; a < I; ++a) xslot_of_arc[a] = fill[fw_pdf[base + a]]++;
-      xpad = (start[num_pdfs] + 1 + 3) & ~3;
-    }
-    d[kXPad] = xpad;
-    const int dummy_slot = xpad - 1;
-    const bool tileable_x = xpad <= 65536;
-    tileable = tileable && tileable_x;
-    d[kTileable] = tileable ? 1 : 0;
     if (tileable) {
-      std::vector<int> iptr(h.in_ptr.end() - (S + 1), h.in_ptr.end());
-      std::vector<int> optr(h.out_ptr.end() - (S + 1), h.out_ptr.end());
-      std::vector<unsigned> iw(I), ow(I);
-      std::vector<double> ip(I), op(I);
       const size_t a0 = size_t(d[kArcOff]);
-      for (int a = 0; a < I; ++a) {
-        iw[a] = unsigned(h.in_src[a0 + a]) | (unsigned(h.in_pdf[a0 + a]) << 16);
-        ip[a] = h.in_p64[a0 + a];
-        ow[a] = unsigned(h.out_dst[a0 + a]) | (unsigned(h.out_pdf[a0 + a]) << 16);
-        op[a] = h.out_p64[a0 + a];
-      }
-      TilePack tf = make_tiles(S, iptr, iw, ip);
-      TilePack tb = make_tiles(S, optr, ow, op);
-      for (size_t k = 0; k < tf.trips.size(); ++k) {
-        h.tf_trips.push_back(tf.trips[k]);
-        h.tf_base.push_back(tf.base[k]);
-        h.tb_trips.push_back(tb.trips[k]);
-        h.tb_base.push_back(tb.base[k]);
-      }
-      h.tf_info.insert(h.tf_info.end(), tf.info.begin(), tf.info.end());
-      h.tb_info.insert(h.tb_info.end(), tb.info.begin(), tb.info.end());
-      while (h.tf_trips.size() % 4) {  // keep per-row tile arrays 16-byte aligned
-        h.tf_trips.push_back(0);
-        h.tf_base.push_back(0);
-        h.tb_trips.push_back(0);
-        h.tb_base.push_back(0);
-        for (int l = 0; l < 32; ++l) {  // info is indexed by tile * 32 + lane
-          h.tf_info.push_back(0xFFFFu);
-          h.tb_info.push_back(0xFFFFu);
+      const int *iptr = &h.in_ptr[h.in_ptr.size() - (S + 1)];
+      const int *optr = &h.out_ptr[h.out_ptr.size() - (S + 1)];
+      TileSchedule tf = schedule_tiles(S, iptr, &h.in_src[a0], &h.in_pdf[a0], &h.in_p64[a0], gl,
+                                       true);
+      TileSchedule tb = schedule_tiles(S, optr, &h.out_dst[a0], &h.out_pdf[a0], &h.out_p64[a0],
+                                       gl, true);
+      std::vector<int> pptr, xslot;
+      int xpad = 0;
+      assign_xslots(tb, &h.out_pdf[a0], num_pdfs, I, 4, pptr, xslot, xpad);
+      tileable = xpad <= 65536;
+      if (tileable) {
+        d[kXPad] = xpad;
+        h.pdf_arc_ptr.insert(h.pdf_arc_ptr.end(), pptr.begin(), pptr.end());
+        for (size_t k = 0; k < tf.trips.size(); ++k) {
+          h.tf_trips.push_back(tf.trips[k]);
+          h.tf_base.push_back(tf.base[k]);
+          h.tb_trips.push_back(tb.trips[k]);
+          h.tb_base.push_back(tb.base[k]);
         }
+        h.tf_info.insert(h.tf_info.end(), tf.info.begin(), tf.info.end());
+        h.tb_info.insert(h.tb_info.end(), tb.info.begin(), tb.info.end());
+        while (h.tf_trips.size() % 4) {  // keep per-row tile arrays 16-byte aligned
+          h.tf_trips.push_back(0);
+          h.tf_base.push_back(0);
+          h.tb_trips.push_back(0);
+          h.tb_base.push_back(0);
+          for (int l = 0; l < 32; ++l) {  // info is indexed by tile * 32 + lane
+            h.tf_info.push_back(0xFFFFu);
+            h.tb_info.push_back(0xFFFFu);
+          }
+        }
+        h.tf_word.insert(h.tf_word.end(), tf.word_idx.begin(), tf.word_idx.end());
+        h.tb_word.insert(h.tb_word.end(), tb.word_idx.begin(), tb.word_idx.end());
+        auto push_wp = [](std::vector<uint2> &dst, const TileSchedule &ts) {
+          for (size_t k = 0; k < ts.prob.size(); ++k) {
+            const float f = float(ts.prob[k]);
+            unsigned bits;
+            std::memcpy(&bits, &f, 4);
+            dst.push_back({ts.word_b32[k], bits});
+          }
+        };
+        push_wp(h.tf_wp, tf);
+        push_wp(h.tb_wp, tb);
+        for (double p : tf.prob) {
+          h.tf_p64.push_back(p);
+          h.tf_p32.push_back(float(p));
+        }
+        for (double p : tb.prob) {
+          h.tb_p64.push_back(p);
+          h.tb_p32.push_back(float(p));
+        }
+        for (int x : xslot) h.tb_xslot.push_back((unsigned short)x);
+        max_xpad = std::max(max_xpad, xpad);
+        d[kTfSlots] = int(tf.word_idx.size());
+        d[kTbSlots] = int(tb.word_idx.size());
+        max_tiles = std::max(max_tiles, int(tf.trips.size()));
+        max_tf = std::max(max_tf, d[kTfSlots]);
+        max_tb = std::max(max_tb, d[kTbSlots]);
       }
-      h.tf_word.insert(h.tf_word.end(), tf.word.begin(), tf.word.end());
-      h.tb_word.insert(h.tb_word.end(), tb.word.begin(), tb.word.end());
-      for (double p : tf.prob) {
-        h.tf_p64.push_back(p);
-        h.tf_p32.push_back(float(p));
-      }
-      for (double p : tb.prob) {
-        h.tb_p64.push_back(p);
-        h.tb_p32.push_back(float(p));
-      }
-      for (int a : tb.arc_of_slot)
-        h.tb_xslot.push_back((unsigned short)(a < 0 ? dummy_slot : xslot_of_arc[a]));
-      // fp32 slots carry byte offsets (index * 4) so the gather addresses are
-      // one shift-add each; requires S, D <= 16383 (checked by kTileable).
-      auto bytes_word = [](unsigned w) {
-        return ((w & 0xFFFFu) << 2) | (((w >> 16) << 2) << 16);
-      };
-      for (size_t k = 0; k < tf.word.size(); ++k) {
-        float f = float(tf.prob[k]);
-        unsigned bits;
-        std::memcpy(&bits, &f, 4);
-        h.tf_wp.push_back({bytes_word(tf.word[k]), bits});
-      }
-      for (size_t k = 0; k < tb.word.size(); ++k) {
-        float f = float(tb.prob[k]);
-        unsigned bits;
-        std::memcpy(&bits, &f, 4);
-        h.tb_wp.push_back({bytes_word(tb.word[k]), bits});
-      }
-      max_xpad = std::max(max_xpad, xpad);
-      d[kTfSlots] = int(tf.word.size());
-      d[kTbSlots] = int(tb.word.size());
-      // tile info arrays are indexed by (tile offset) * 32 + lane
-      max_tiles = std::max(max_tiles, int(tf.trips.size()));
-      max_tf = std::max(max_tf, d[kTfSlots]);
-      max_tb = std::max(max_tb, d[kTbSlots]);
-    } else {
+    }
+    d[kTileable] = tileable ? 1 : 0;
+    if (!tileable) {
       all_tileable = false;
     }
   }
@@ -383,6 +309,10 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   g->max_tb_slots = max_tb;
   g->tileable = all_tileable;
   g->max_xpad = max_xpad;
+  g->rep_r = gl.rep_r;
+  g->r_stride = gl.r_stride;
+  g->rep_e = gl.rep_e;
+  g->e_stride = gl.e_stride;
   DevGraphs &dv = g->dev;
   std::vector<Piece> pieces;
   auto add = [&](const auto &vec, const auto **dst) {

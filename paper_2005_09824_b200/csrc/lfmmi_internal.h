@@ -72,6 +72,7 @@ struct lfmmi_graphs {
   int32_t max_chunks = 0, max_in_deg = 0, max_out_deg = 0;
   int32_t max_tiles = 0, max_tf_slots = 0, max_tb_slots = 0, max_xpad = 0;
   bool tileable = false;
+  int32_t rep_r = 1, r_stride = 0, rep_e = 1, e_stride = 0;  // gather-vector replication
   void *device_block = nullptr;
   size_t device_bytes = 0;
   lfmmi::DevGraphs dev{};

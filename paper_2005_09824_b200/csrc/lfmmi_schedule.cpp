@@ -1,0 +1,214 @@
+// Offline, bank-conflict-aware scheduling of the tile packs (host side).
+//
+// A tile packs 32 states (one per lane, sorted by degree); slot row j of the
+// tile is one warp-wide step: lane l processes one of its state's arcs.  Each
+// step gathers vec[gidx] (alpha column in the forward, beta column in the
+// backward) and e[pdf] from shared memory, and the backward additionally
+// stores one posterior term.  A warp-wide shared access costs one wavefront
+// per distinct address in its busiest bank, so random gathers cost ~3.5x the
+// ideal.  Three free choices remove most of that:
+//   * the order of each lane's arcs across slot rows (any permutation is
+//     valid: the per-state sum just changes order);
+//   * which copy of a replicated gather vector an arc reads (the kernel keeps
+//     rep_r copies of the alpha/beta column and rep_e copies of the emission
+//     row at strides that shift every copy by a fixed number of banks);
+//   * where in its pdf group each posterior term is stored.
+// The greedy below fills each slot row lane by lane (fewest remaining arcs
+// first), picking the arc and copies that add the fewest new addresses to
+// already-used banks.  Broadcasts (same address) are free.
+#include "lfmmi_schedule.h"
+
+#include <algorithm>
+#include <numeric>
+
+namespace lfmmi {
+
+namespace {
+
+struct BankSet {  // distinct addresses per bank within one slot row
+  int n[32];
+  int addr[32][8];
+  void clear() { std::fill(n, n + 32, 0); }
+  int cost(int a) const {
+    const int b = a & 31;
+    for (int k = 0; k < n[b]; ++k)
+      if (addr[b][k] == a) return 0;
+    return n[b];
+  }
+  void add(int a) {
+    const int b = a & 31;
+    for (int k = 0; k < n[b]; ++k)
+      if (addr[b][k] == a) return;
+    if (n[b] < 8) addr[b][n[b]] = a;
+    n[b] = std::min(n[b] + 1, 8);
+  }
+};
+
+}  // namespace
+
+GatherLayout make_gather_layout(int max_states, int num_pdfs) {
+  GatherLayout gl;
+  auto round32 = [](int x) { return (x + 31) & ~31; };
+  gl.r_stride = round32(max_states) + 16;  // copy 1 sits 16 banks over
+  gl.rep_r = (2 * gl.r_stride <= 16383) ? 2 : 1;
+  if (gl.rep_r == 1) gl.r_stride = (max_states + 3) & ~3;
+  gl.e_stride = round32(num_pdfs) + 8;  // copies shift by 8 banks
+  gl.rep_e = 4;
+  while (gl.rep_e > 1 && gl.rep_e * gl.e_stride > 16383) gl.rep_e >>= 1;
+  if (gl.rep_e == 1) gl.e_stride = (num_pdfs + 3) & ~3;
+  return gl;
+}
+
+TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
+                            const double *prob, const GatherLayout &gl, bool optimize) {
+  TileSchedule ts;
+  std::vector<int> order(S);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    return (ptr[x + 1] - ptr[x]) > (ptr[y + 1] - ptr[y]);
+  });
+  const int ntiles = (S + 31) / 32;
+  int base = 0;
+  BankSet rb, eb;
+  for (int w = 0; w < ntiles; ++w) {
+    std::vector<std::vector<int>> rem(32);
+    int trips = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int k = 32 * w + l;
+      if (k >= S) {
+        ts.info.push_back(0xFFFFu);
+        continue;
+      }
+      const int s = order[k];
+      const int deg = ptr[s + 1] - ptr[s];
+      ts.info.push_back(unsigned(s) | (unsigned(deg) << 16));
+      for (int a = ptr[s]; a < ptr[s + 1]; ++a) rem[l].push_back(a);
+      trips = std::max(trips, deg);
+    }
+    ts.trips.push_back(trips);
+    ts.base.push_back(base);
+    const size_t start = ts.arc.size();
+    ts.arc.resize(start + size_t(32) * trips, -1);
+    ts.word_idx.resize(start + size_t(32) * trips, 0u);
+    ts.word_b32.resize(start + size_t(32) * trips, 0u);
+    ts.prob.resize(start + size_t(32) * trips, 0.0);
+    std::vector<int> lanes;
+    for (int j = 0; j < trips; ++j) {
+      rb.clear();
+      eb.clear();
+      lanes.clear();
+      for (int l = 0; l < 32; ++l)
+        if (!rem[l].empty()) lanes.push_back(l);
+      std::stable_sort(lanes.begin(), lanes.end(),
+                       [&](int x, int y) { return rem[x].size() < rem[y].size(); });
+      unsigned pad_idx = 0, pad_b32 = 0;
+      bool have_pad = false;
+      for (int l : lanes) {
+        int best = 0, best_cost = 1 << 30, best_cr = 0, best_ce = 0;
+        const int ncand = optimize ? int(rem[l].size()) : 1;
+        for (int c = 0; c < ncand; ++c) {
+          const int a = rem[l][c];
+          int rc = 1 << 20, cr_best = 0;
+          for (int cr = 0; cr < gl.rep_r; ++cr) {
+            const int v = rb.cost(cr * gl.r_stride + gidx[a]);
+            if (v < rc) {
+              rc = v;
+              cr_best = cr;
+            }
+          }
+          int ec = 1 << 20, ce_best = 0;
+          for (int ce = 0; ce < gl.rep_e; ++ce) {
+            const int v = eb.cost(ce * gl.e_stride + pdf[a]);
+            if (v < ec) {
+              ec = v;
+              ce_best = ce;
+            }
+          }
+          if (!optimize) rc = ec = 0, cr_best = ce_best = 0;
+          if (rc + ec < best_cost) {
+            best_cost = rc + ec;
+            best = c;
+            best_cr = cr_best;
+            best_ce = ce_best;
+          }
+        }
+        const int a = rem[l][best];
+        rem[l].erase(rem[l].begin() + best);
+        const int ra = best_cr * gl.r_stride + gidx[a];
+        const int ea = best_ce * gl.e_stride + pdf[a];
+        rb.add(ra);
+        eb.add(ea);
+        const size_t slot = start + size_t(32) * j + l;
+        ts.arc[slot] = a;
+        ts.prob[slot] = prob[a];
+        ts.word_idx[slot] = unsigned(gidx[a]) | (unsigned(pdf[a]) << 16);
+        ts.word_b32[slot] = (unsigned(ra) << 2) | ((unsigned(ea) << 2) << 16);
+        if (!have_pad) {
+          pad_idx = ts.word_idx[slot];
+          pad_b32 = ts.word_b32[slot];
+          have_pad = true;
+        }
+      }
+      // Idle lanes re-read an address already used in this row (a free
+      // broadcast) with probability 0.
+      for (int l = 0; l < 32; ++l) {
+        const size_t slot = start + size_t(32) * j + l;
+        if (ts.arc[slot] < 0) {
+          ts.word_idx[slot] = pad_idx;
+          ts.word_b32[slot] = pad_b32;
+        }
+      }
+    }
+    base += 32 * trips;
+  }
+  return ts;
+}
+
+void assign_xslots(const TileSchedule &tb, const int *pdf_of_arc, int num_pdfs, int num_arcs,
+                   int slack, std::vector<int> &pdf_ptr, std::vector<int> &xslot_of_slot,
+                   int &xpad) {
+  std::vector<int> cnt(num_pdfs, 0);
+  for (int a = 0; a < num_arcs; ++a) cnt[pdf_of_arc[a]]++;
+  pdf_ptr.assign(num_pdfs + 1, 0);
+  for (int p = 0; p < num_pdfs; ++p)
+    pdf_ptr[p + 1] = pdf_ptr[p] + (cnt[p] ? ((cnt[p] + slack + 3) & ~3) : 0);
+  const int dummy = pdf_ptr[num_pdfs];
+  xpad = (dummy + 1 + 3) & ~3;
+  // free positions per (pdf, bank)
+  std::vector<std::vector<int>> freel(size_t(num_pdfs) * 32);
+  for (int p = 0; p < num_pdfs; ++p)
+    for (int pos = pdf_ptr[p + 1] - 1; pos >= pdf_ptr[p]; --pos)
+      freel[size_t(p) * 32 + (pos & 31)].push_back(pos);
+  xslot_of_slot.assign(tb.arc.size(), dummy);
+  for (size_t w = 0; w < tb.trips.size(); ++w) {
+    for (int j = 0; j < tb.trips[w]; ++j) {
+      bool used[32] = {false};
+      const size_t row = size_t(tb.base[w]) + size_t(32) * j;
+      for (int l = 0; l < 32; ++l)
+        if (tb.arc[row + l] < 0) used[dummy & 31] = true;
+      for (int l = 0; l < 32; ++l) {
+        const int a = tb.arc[row + l];
+        if (a < 0) continue;
+        const int p = pdf_of_arc[a];
+        int bank = -1, bank_any = -1;
+        size_t most = 0;
+        for (int b = 0; b < 32; ++b) {
+          const size_t nfree = freel[size_t(p) * 32 + b].size();
+          if (!nfree) continue;
+          if (bank_any < 0) bank_any = b;
+          if (!used[b] && nfree > most) {
+            most = nfree;
+            bank = b;
+          }
+        }
+        if (bank < 0) bank = bank_any;
+        auto &fl = freel[size_t(p) * 32 + bank];
+        xslot_of_slot[row + l] = fl.back();
+        fl.pop_back();
+        used[bank] = true;
+      }
+    }
+  }
+}
+
+}  // namespace lfmmi

@@ -1,0 +1,37 @@
+// Host-side tile scheduling (see lfmmi_schedule.cpp).
+#pragma once
+
+#include <vector>
+
+namespace lfmmi {
+
+// Replication of the shared-memory gather vectors: copy c of the alpha/beta
+// column sits at c * r_stride, copy c of the emission row at c * e_stride
+// (floats), strides chosen so every copy is shifted by a fixed bank offset.
+struct GatherLayout {
+  int rep_r = 1, r_stride = 0, rep_e = 1, e_stride = 0;
+};
+
+GatherLayout make_gather_layout(int max_states, int num_pdfs);
+
+struct TileSchedule {
+  std::vector<unsigned> info;      // per tile lane: state | degree << 16 (0xFFFF = none)
+  std::vector<int> trips, base;    // per tile
+  std::vector<int> arc;            // per slot: CSR arc index (-1 = padding)
+  std::vector<unsigned> word_idx;  // gidx | pdf << 16 (plain indices; f64 path)
+  std::vector<unsigned> word_b32;  // byte offsets incl. the chosen copies (f32 path)
+  std::vector<double> prob;        // 0 on padding
+};
+
+// ptr: CSR row pointers (S + 1) of the layout; gidx/pdf/prob per CSR arc.
+TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
+                            const double *prob, const GatherLayout &gl, bool optimize);
+
+// Posterior slot of every backward tile slot: pdf groups (16-byte aligned,
+// `slack` spare positions each), conflict-avoiding positions per slot row,
+// padding slots -> one trailing dummy slot.  pdf_of_arc is indexed by CSR arc.
+void assign_xslots(const TileSchedule &tb, const int *pdf_of_arc, int num_pdfs, int num_arcs,
+                   int slack, std::vector<int> &pdf_ptr, std::vector<int> &xslot_of_slot,
+                   int &xpad);
+
+}  // namespace lfmmi

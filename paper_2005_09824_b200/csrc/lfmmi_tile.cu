@@ -75,7 +75,7 @@ __device__ __forceinline__ double sum_groups4(const double *x, int n4) {
 
 __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int ntiles, int D,
                                                   int X_pad, int S_pad, int D_pad, int T_pad,
-                                                  int NW, int real) {
+                                                  int RB, int EB, int real) {
   TileLayout l;
   size_t o = 512;  // scratch: 32 doubles + 32 int64
   const size_t F = smem_graph ? size_t(Fmax) : 0;
@@ -86,10 +86,10 @@ __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int
   l.ttrips = o;  o = al16(o + size_t(pad4(int(nt))) * 4);
   l.tbase = o;   o = al16(o + size_t(pad4(int(nt))) * 4);
   l.pdfptr = o;  o = al16(o + size_t(D + 1) * 4);
-  l.xterm = o;   o = al16(o + size_t(2) * X_pad * real);
-  l.rbuf = o;    o = al16(o + size_t(2) * S_pad * real);
+  l.xterm = o;   o = al16(o + size_t(X_pad) * real);      // posterior slots (one frame)
+  l.rbuf = o;    o = al16(o + size_t(2) * RB * real);     // alpha/beta columns x copies
   l.aring = o;   o = al16(o + size_t(2) * S_pad * real);
-  l.ebuf = o;    o = al16(o + size_t(2) * D_pad * real);
+  l.ebuf = o;    o = al16(o + size_t(2) * EB * real);     // emission rows x copies
   l.stage = o;   o = al16(o + size_t(4) * D_pad * real);
   l.gstage = o;  o = al16(o + size_t(2) * D_pad * real);
   l.scales = o;  o = al16(o + size_t(T_pad) * real);
@@ -97,7 +97,6 @@ __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int
   l.part = o;    o = al16(o + size_t(2) * 32 * real);
   l.mpart = o;   o = al16(o + size_t(2) * 32 * real);
   l.total = o;
-  (void)NW;
   return l;
 }
 
@@ -253,8 +252,9 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   (void)ntile_rounds_max;
   const int b = blockIdx.x * IPC + gid;
   if (b >= a.B) return;  // whole group exits together (no CTA-wide barriers for IPC > 1)
+  const int RB = a.rep_r * a.r_stride, EB = a.rep_e * a.e_stride;
   const TileLayout lay = tile_layout(SMEM_GRAPH, Fmax, ntiles_max, a.D, X_pad, a.S_pad, a.D_pad,
-                                     a.T_pad, NW, int(sizeof(Real)));
+                                     a.T_pad, RB, EB, int(sizeof(Real)));
   unsigned char *smem = smem_all + lay.total * gid;
   double *dscr = reinterpret_cast<double *>(smem);
   long long *lscr = reinterpret_cast<long long *>(smem + 256);
@@ -404,13 +404,20 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       m = warp_max(m);
     }
     const Real *src = stage + (t & 3) * D_pad;
-    Real *dst = ebuf + (t & 1) * D_pad;
-    for (int d = ctid; d < D; d += GROUP) dst[d] = exp_r(src[d] - m);
+    Real *dst = ebuf + (t & 1) * EB;
+    for (int d = ctid; d < D; d += GROUP) {
+      const Real v = exp_r(src[d] - m);
+      for (int c = 0; c < a.rep_e; ++c) dst[c * a.e_stride + d] = v;
+    }
     if (record_shift && ctid == 0) shifts[t] = m;
   };
 
+  // alpha/beta columns are replicated (rep_r copies, see lfmmi_schedule.cpp)
+  auto put_vec = [&](Real *v, int s, Real x) {
+    for (int c = 0; c < a.rep_r; ++c) v[c * a.r_stride + s] = x;
+  };
   // ---- prologue -----------------------------------------------------------------
-  for (int s = tid; s < S; s += GROUP) rbuf[s] = (s == init) ? Real(1) : Real(0);
+  for (int s = tid; s < S; s += GROUP) put_vec(rbuf, s, (s == init) ? Real(1) : Real(0));
   issue_row(0);
   issue_row(1);
   cp_async_commit();
@@ -442,7 +449,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       if (tid == 0) scales[k - 1] = t2;
     }
     {
-      const Real *r = rbuf + cur * S_pad;
+      const Real *r = rbuf + cur * RB;
       Real *arow = trellis + size_t(k) * S_pad;
       if constexpr (CUSTOM_PI) {
         for (int s = tid; s < S; s += GROUP) arow[s] = (r[s] + leakc * pi[s]) * inv2;
@@ -455,9 +462,9 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     issue_row(k + 2);
     cp_async_commit();
     {
-      const Real *e = ebuf + cur * D_pad;
-      const Real *r = rbuf + cur * S_pad;
-      Real *rn = rbuf + nxt * S_pad;
+      const Real *e = ebuf + cur * EB;
+      const Real *r = rbuf + cur * RB;
+      Real *rn = rbuf + nxt * RB;
       const bool last = (k + 1 == T);
       const uint32_t e32 = smem_u32(e), r32 = smem_u32(r);
       (void)e32;
@@ -485,8 +492,8 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
             const Real w = p * e[wd >> 16];
             const int src = int(wd & 0xFFFFu);
             A = fma(w, r[src], A);
-            if constexpr (CUSTOM_PI)
-              Bs = fma(w, pi[src], Bs);
+            if constexpr (CUSTOM_PI)  // gather index may name copy 1 (rep_r <= 2)
+              Bs = fma(w, pi[src >= a.r_stride ? src - a.r_stride : src], Bs);
             else
               Bs += w;
           }
@@ -503,7 +510,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
         if (s != 0xFFFF) {
           Real raw = inv2 * (A + leakc * (CUSTOM_PI ? Bs : upi * Bs));
           if (last) raw *= fin[s];
-          rn[s] = raw;
+          put_vec(rn, s, raw);
           psum += raw;
         }
       }
@@ -566,7 +573,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     const int *pp = a.g.pdf_arc_ptr + desc[kPdfPtrOff2];
     for (int d = tid; d <= D; d += GROUP) pdfptr[d] = pp[d];
     // Padding slots of the per-pdf groups are never written: zero them once.
-    for (int i = tid; i < 2 * X_pad; i += GROUP) xterm[i] = Real(0);
+    for (int i = tid; i < X_pad; i += GROUP) xterm[i] = Real(0);
   }
   auto issue_alpha = [&](int k) {
     if (k < 0) return;
@@ -579,22 +586,35 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     Real *dst = gstage + (t & 1) * D_pad;
     for (int d = ctid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
   };
-  // gamma_t[d] = sum of pdf d's slots (float4 loads, 4 accumulators).
-  auto flush_post = [&](int t, const Real *xt) {
+  // gamma_t[d] = sum of pdf d's slots: SPL chore lanes per pdf, each summing
+  // float4 groups, combined by a shuffle within the SPL-lane segment.
+  int spl = 1;
+  while (spl < 32 && D * spl * 2 <= GROUP) spl <<= 1;
+  auto flush_post = [&](int t) {
     Real *prow = post_b + size_t(t) * D;
     const Real *old = gstage + (t & 1) * D_pad;
-    for (int d = ctid; d < D; d += GROUP) {
-      const Real g = sum_groups4(xt + pdfptr[d], (pdfptr[d + 1] - pdfptr[d]) >> 2);
-      switch (mode) {
-        case kPostNegate: prow[d] = -g; break;
-        case kPostAdd: prow[d] = old[d] + g; break;
-        case kPostSubtract: prow[d] = old[d] - g; break;
-        default: prow[d] = g;
+    const int sub = ctid & (spl - 1);
+    for (int base_i = 0; base_i < D * spl; base_i += GROUP) {
+      const int idx = base_i + ctid;
+      const int d = idx / spl;
+      Real g = Real(0);
+      if (d < D) {
+        const int lo = pdfptr[d] >> 2, hi = pdfptr[d + 1] >> 2;
+        for (int q = lo + sub; q < hi; q += spl) g += sum_groups4(xterm + 4 * q, 1);
+      }
+      for (int o = 1; o < spl; o <<= 1) g += __shfl_xor_sync(kFull, g, o);
+      if (d < D && sub == 0) {
+        switch (mode) {
+          case kPostNegate: prow[d] = -g; break;
+          case kPostAdd: prow[d] = old[d] + g; break;
+          case kPostSubtract: prow[d] = old[d] - g; break;
+          default: prow[d] = g;
+        }
       }
     }
   };
 
-  for (int s = tid; s < S; s += GROUP) rbuf[(T & 1) * S_pad + s] = fin[s] * (Real(1) + lam);
+  for (int s = tid; s < S; s += GROUP) put_vec(rbuf + (T & 1) * RB, s, fin[s] * (Real(1) + lam));
   issue_row(T - 1);
   issue_row(T - 2);
   issue_alpha(T - 1);
@@ -611,18 +631,17 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     Real ld = Real(0);
     if (t < T && lam > Real(0)) ld = lam * lane_sum<NW>(part + ct * 32, lane);
     const Real inv = Real(1) / scales[t - 1];
-    if (t < T) flush_post(t, xterm + ct * X_pad);
     if (t - 2 >= 0) compute_e(t - 2, false);
     issue_row(t - 3);
     issue_alpha(t - 2);
     issue_post(t - 1);
     cp_async_commit();
     {
-      const Real *bt = rbuf + ct * S_pad;
-      const Real *e = ebuf + cp * D_pad;
+      const Real *bt = rbuf + ct * RB;
+      const Real *e = ebuf + cp * EB;
       const Real *al = aring + cp * S_pad;  // alpha_{t-1}
-      Real *bn = rbuf + cp * S_pad;
-      Real *xt = xterm + cp * X_pad;
+      Real *bn = rbuf + cp * RB;
+      Real *xt = xterm;
       Real dp = Real(0);
       for (int rr = 0; rr < nrounds; ++rr) {
         const int tile = tile_of(rr);
@@ -649,7 +668,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
         }
         if (s != 0xFFFF) {
           const Real v = inv * A;
-          bn[s] = v;
+          put_vec(bn, s, v);
           dp = fma(CUSTOM_PI ? pi[s] : upi, v, dp);
         }
       }
@@ -659,8 +678,11 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     cp_async_wait<0>();
     row_max_part(t - 3);
     gsync();
+    // The posterior slots of frame t-1 are complete: write its gradient row,
+    // then release the (single) slot buffer for the next frame.
+    if (cwarp * 32 < D * spl) flush_post(t - 1);
+    gsync();
   }
-  flush_post(0, xterm);
 }
 
 template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI>
@@ -700,11 +722,12 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
   const int X_pad = pad4(std::max(4, g->max_xpad));
   const int real = int(sizeof(Real));
   if (warp_per_item) {
+    const int RB = a.rep_r * a.r_stride, EB = a.rep_e * a.e_stride;
     const size_t per = tile_layout(false, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
-                                   a.T_pad, 1, real).total;
+                                   a.T_pad, RB, EB, real).total;
     // Several utterances per CTA, but keep at least ~one CTA per SM busy.
     const size_t per_s = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
-                                     a.T_pad, 1, real).total;
+                                     a.T_pad, RB, EB, real).total;
     const bool many = a.B >= 8 * 148;
     if (many && per_s * 8 <= size_t(kMaxSmem))
       return launch_tile_impl<Real, 32, 8, true>(a, g, per_s, st);
@@ -715,7 +738,7 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     return set_error(LFMMI_ERR_UNSUPPORTED, "numerator slice exceeds shared memory");
   }
   const size_t per = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
-                                 a.T_pad, kDenGroup / 32, real).total;
+                                 a.T_pad, a.rep_r * a.r_stride, a.rep_e * a.e_stride, real).total;
   if (per > size_t(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "tile pack needs " + std::to_string(per) + " B shared memory");
