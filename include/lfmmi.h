@@ -51,6 +51,12 @@ const char *lfmmi_last_error(void);
 const char *lfmmi_version(void);
 
 /*
+ * Number of kernels the last successful lfmmi_chain_loss call on this thread
+ * launched (1 = fused single-launch path, 4 = two-pass path).  Diagnostic.
+ */
+int32_t lfmmi_last_launch_count(void);
+
+/*
  * Build a device-resident graph batch from the reference's padded host
  * layout (graph.py:253-279).  G physical rows; row r has row_num_states[r]
  * states and row_num_arcs[r] arcs.  Arrays are (G, max_arcs) in the

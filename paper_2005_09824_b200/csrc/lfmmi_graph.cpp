@@ -13,6 +13,7 @@
 //           scatter over all arcs, _kernels.py:211-224, by a deterministic
 //           per-pdf gather).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -62,6 +63,7 @@ struct HostPack {
   std::vector<double> fin64;
   std::vector<unsigned> tf_info, tb_info, tf_word, tb_word;
   std::vector<int> tf_trips, tf_base, tb_trips, tb_base, pdf_arc_ptr;
+  std::vector<int> tf_wlist, tb_wlist, tf_wtab, tb_wtab;
   std::vector<float> tf_p32, tb_p32;
   std::vector<double> tf_p64, tb_p64;
   std::vector<unsigned short> tb_xslot;
@@ -243,9 +245,36 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           h.tb_trips.push_back(tb.trips[k]);
           h.tb_base.push_back(tb.base[k]);
         }
+        {
+          // Warp lists for the 16-warp CTA kernels: the last warps carry the
+          // per-frame emission-row chores, so they start with a small bias.
+          std::vector<int> bias(kTableNW, 0), tab, lst;
+          const int chore = std::min(kTableNW, (num_pdfs + 31) / 32);
+          for (int w = kTableNW - chore; w < kTableNW; ++w) bias[w] = 2;
+          d[kWTabOff] = int(h.tf_wtab.size());
+          warp_lists(tf.trips, bias, tab, lst);
+          h.tf_wtab.insert(h.tf_wtab.end(), tab.begin(), tab.end());
+          h.tf_wlist.insert(h.tf_wlist.end(), lst.begin(), lst.end());
+          // Backward: the top warps also flush the gradient row of the previous
+          // frame (fb_chain_kernel, spl lanes per pdf, ~5 instructions per float4
+          // of posterior slots vs ~14 per arc-slot row).
+          int spl = 1;
+          while (spl < 32 && num_pdfs * spl * 2 <= 32 * kTableNW) spl <<= 1;
+          const int lanes = num_pdfs * spl;
+          if (lanes < 32 * kTableNW && !std::getenv("LFMMI_NO_FLUSH_BIAS")) {
+            const int fw = (lanes + 31) / 32;
+            const int per_lane = (xpad / 4 + lanes - 1) / lanes;
+            for (int w = kTableNW - fw; w < kTableNW; ++w) bias[w] += (per_lane * 5 + 13) / 14;
+          }
+          warp_lists(tb.trips, bias, tab, lst);
+          h.tb_wtab.insert(h.tb_wtab.end(), tab.begin(), tab.end());
+          h.tb_wlist.insert(h.tb_wlist.end(), lst.begin(), lst.end());
+        }
         h.tf_info.insert(h.tf_info.end(), tf.info.begin(), tf.info.end());
         h.tb_info.insert(h.tb_info.end(), tb.info.begin(), tb.info.end());
         while (h.tf_trips.size() % 4) {  // keep per-row tile arrays 16-byte aligned
+          h.tf_wlist.push_back(0);
+          h.tb_wlist.push_back(0);
           h.tf_trips.push_back(0);
           h.tf_base.push_back(0);
           h.tb_trips.push_back(0);
@@ -343,6 +372,10 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   add(h.tf_info, &dv.tf_info);
   add(h.tb_info, &dv.tb_info);
   add(h.tf_trips, &dv.tf_trips);
+  add(h.tf_wlist, &dv.tf_wlist);
+  add(h.tb_wlist, &dv.tb_wlist);
+  add(h.tf_wtab, &dv.tf_wtab);
+  add(h.tb_wtab, &dv.tb_wtab);
   add(h.tf_base, &dv.tf_base);
   add(h.tb_trips, &dv.tb_trips);
   add(h.tb_base, &dv.tb_base);

@@ -32,16 +32,20 @@ struct GroupLayout {
   int rbuf, aring, ebuf, stage, gstage, slots, scales, shifts, part, mpart, reals;
 };
 
+// LARGE (graphs whose state vectors leave no room for the alpha ring, e.g.
+// 20k states): alpha_{t-1} is read straight from the HBM/L2 trellis, the
+// gradient is never read back (WRITE / NEGATE modes only) and the per-chunk
+// posterior partials are single-buffered (one extra barrier per frame).
 __host__ __device__ inline GroupLayout group_layout(int S_pad, int D_pad, int NC_pad, int T_pad,
-                                                    int NW) {
+                                                    int NW, bool large = false) {
   GroupLayout l;
   int o = 0;
-  l.rbuf = o;   o += 2 * S_pad;   // alpha / beta columns (ping-pong)
-  l.aring = o;  o += 3 * S_pad;   // alpha columns streamed back from HBM
-  l.ebuf = o;   o += 2 * D_pad;   // exp'd emission rows
-  l.stage = o;  o += 4 * D_pad;   // raw log-likelihood rows (cp.async ring)
-  l.gstage = o; o += 3 * D_pad;   // existing gradient rows (ADD / SUBTRACT modes)
-  l.slots = o;  o += 2 * NC_pad;  // per-chunk posterior partials
+  l.rbuf = o;   o += 2 * S_pad;                  // alpha / beta columns (ping-pong)
+  l.aring = o;  o += large ? 0 : 3 * S_pad;      // alpha columns streamed back from HBM
+  l.ebuf = o;   o += 2 * D_pad;                  // exp'd emission rows
+  l.stage = o;  o += 4 * D_pad;                  // raw log-likelihood rows (cp.async ring)
+  l.gstage = o; o += large ? 0 : 3 * D_pad;      // existing gradient rows (ADD / SUBTRACT modes)
+  l.slots = o;  o += (large ? 1 : 2) * NC_pad;   // per-chunk posterior partials
   l.scales = o; o += T_pad;
   l.shifts = o; o += T_pad;
   l.part = o;   o += pad4(2 * NW);
@@ -53,12 +57,13 @@ __host__ __device__ inline GroupLayout group_layout(int S_pad, int D_pad, int NC
 constexpr int kGroupScratch = 512;
 
 template <typename Real>
-size_t group_smem_bytes(int S_pad, int D_pad, int NC_pad, int T_pad, int group) {
-  const GroupLayout l = group_layout(S_pad, D_pad, NC_pad, T_pad, group / 32);
+size_t group_smem_bytes(int S_pad, int D_pad, int NC_pad, int T_pad, int group,
+                        bool large = false) {
+  const GroupLayout l = group_layout(S_pad, D_pad, NC_pad, T_pad, group / 32, large);
   return (kGroupScratch + size_t(l.reals) * sizeof(Real) + 15) & ~size_t(15);
 }
 
-template <typename Real, int GROUP, int GPC>
+template <typename Real, int GROUP, int GPC, bool LARGE>
 __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Real> a) {
   constexpr int NW = GROUP / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -67,7 +72,7 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
   const int b = blockIdx.x * GPC + gid;
   if (b >= a.B) return;  // whole group exits together
 
-  const GroupLayout lay = group_layout(a.S_pad, a.D_pad, a.NC_pad, a.T_pad, NW);
+  const GroupLayout lay = group_layout(a.S_pad, a.D_pad, a.NC_pad, a.T_pad, NW, LARGE);
   const size_t gbytes = (kGroupScratch + size_t(lay.reals) * sizeof(Real) + 15) & ~size_t(15);
   unsigned char *base = smem_raw + gbytes * gid;
   double *dscr = reinterpret_cast<double *>(base);
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
 
   // ---- backward + fused posterior / gradient ------------------------------------
   auto issue_alpha = [&](int k) {
-    if (k < 0) return;
+    if (LARGE || k < 0) return;
     const char *src = reinterpret_cast<const char *>(trellis + size_t(k) * S_pad);
     char *d = reinterpret_cast<char *>(aring + (k % 3) * S_pad);
     const int chunks = S_pad * int(sizeof(Real)) / 16;
@@ -353,7 +358,8 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
       ld = lam * dot;
     }
     const Real inv = Real(1) / scales[t - 1];
-    if (t < T) flush_post(t, slots + ct * NC_pad);
+    if (t < T) flush_post(t, slots + (LARGE ? 0 : ct * NC_pad));
+    if (LARGE) gsync();  // single slot buffer: flush before the next frame's partials
     if (t - 2 >= 0) compute_e(t - 2, false);
     issue_row(t - 4);
     issue_alpha(t - 3);
@@ -381,8 +387,8 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
       if (lane == 0) part[cp * NW + warp] = dp;
     }
     {
-      const Real *al = aring + ((t - 1) % 3) * S_pad;
-      Real *sl = slots + cp * NC_pad;
+      const Real *al = LARGE ? trellis + size_t(t - 1) * S_pad : aring + ((t - 1) % 3) * S_pad;
+      Real *sl = slots + (LARGE ? 0 : cp * NC_pad);
       for (int c = tid; c < nch; c += GROUP) {
         const int lo = __ldg(ch_begin + c), hi = __ldg(ch_end + c);
         Real P = Real(0), Q = Real(0);
@@ -403,23 +409,23 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
 }
 
 // ---- host-side launcher --------------------------------------------------------
-template <typename Real, int GROUP, int GPC>
+template <typename Real, int GROUP, int GPC, bool LARGE = false>
 static int launch_group_impl(const FBArgs<Real> &a, cudaStream_t st) {
-  const size_t per = group_smem_bytes<Real>(a.S_pad, a.D_pad, a.NC_pad, a.T_pad, GROUP);
+  const size_t per = group_smem_bytes<Real>(a.S_pad, a.D_pad, a.NC_pad, a.T_pad, GROUP, LARGE);
   const size_t smem = per * GPC;
   if (smem > size_t(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED, "utterance/graph too large for the group kernel (" +
                                                 std::to_string(smem) + " B shared memory)");
   static bool configured = false;
   if (!configured) {
-    int rc = check_cuda(cudaFuncSetAttribute(fb_group_kernel<Real, GROUP, GPC>,
+    int rc = check_cuda(cudaFuncSetAttribute(fb_group_kernel<Real, GROUP, GPC, LARGE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
                         "cudaFuncSetAttribute(group)");
     if (rc) return rc;
     configured = true;
   }
   const int grid = (a.B + GPC - 1) / GPC;
-  fb_group_kernel<Real, GROUP, GPC><<<grid, GROUP * GPC, smem, st>>>(a);
+  fb_group_kernel<Real, GROUP, GPC, LARGE><<<grid, GROUP * GPC, smem, st>>>(a);
   return check_cuda(cudaGetLastError(), "fb_group_kernel launch");
 }
 
@@ -436,7 +442,15 @@ int launch_group(const FBArgs<Real> &a, int group, cudaStream_t st) {
     case 128: return launch_group_impl<Real, 128, 1>(a, st);
     case 256: return launch_group_impl<Real, 256, 1>(a, st);
     case 512: return launch_group_impl<Real, 512, 1>(a, st);
-    default: return launch_group_impl<Real, 1024, 1>(a, st);
+    default: {
+      const int rc = launch_group_impl<Real, 1024, 1>(a, st);
+      // Graphs too large for the alpha ring (config 4: 20k states) stream alpha
+      // from L2 instead; the gradient is then written, never read back.
+      const bool reads_post = a.mode == kPostAdd || a.mode == kPostSubtract;
+      if (rc == LFMMI_ERR_UNSUPPORTED && !reads_post)
+        return launch_group_impl<Real, 1024, 1, true>(a, st);
+      return rc;
+    }
   }
 }
 

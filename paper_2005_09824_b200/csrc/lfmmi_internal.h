@@ -33,6 +33,7 @@ enum DescField : int {
   kPdfPtrOff2 = 16,  // offset into pdf_arc_ptr (D + 1 per row): posterior slot groups
   kTileable = 17,    // 1 if indices fit the 16-bit tile encoding
   kXPad = 18,        // posterior slot count incl. per-pdf padding + dummy slot (multiple of 4)
+  kWTabOff = 19,     // offset into the per-phase warp tables (kWarpTable ints per row)
   kDescInts = 20
 };
 
@@ -57,6 +58,8 @@ struct DevGraphs {
   // tile packs
   const unsigned *tf_info, *tb_info;  // per tile lane: state | degree << 16
   const int *tf_trips, *tf_base, *tb_trips, *tb_base;
+  const int *tf_wlist, *tb_wlist;     // tile ids grouped by warp (16-warp LPT schedule)
+  const int *tf_wtab, *tb_wtab;       // per-warp ranges + warps by ascending load
   const unsigned *tf_word, *tb_word;  // src|pdf<<16 (forward), dst|pdf<<16 (backward)
   const float *tf_p32, *tb_p32;
   const double *tf_p64, *tb_p64;

@@ -22,4 +22,31 @@ template <typename Real>
 int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *graphs, bool warp_per_item,
                 cudaStream_t st);
 
+// Fused LF-MMI loss (lfmmi_chain.cu): numerator + denominator + gradient in one CTA.
+struct ChainArgs {
+  DevGraphs den, num;
+  const int64_t *den_row_map, *num_row_map;
+  int B, T_max, D, D_pad, T_pad;
+  int Sd_pad, Sn_pad;  // trellis row strides
+  int rep_rd, r_strided, rep_rn, r_striden, rep_e, e_stride;
+  const float *L;
+  const int *lengths;
+  float leak, floor_eff;
+  float *trellis_d, *trellis_n;
+  float *grad;
+  double *num_lp, *den_lp;
+  int *num_fail, *den_fail;
+  double *totals;
+  unsigned *counter;
+  long long *prof;  // debug section timers (LFMMI_PROFILE), normally NULL
+  int ablate;       // debug ablation bits (LFMMI_ABLATE, profiled launches only)
+};
+
+struct ChainDims {
+  int Fd, ntd, Xd;  // denominator: max slots per phase, tiles, posterior slots
+  int Fn, ntn, Xn;  // numerator
+};
+
+int launch_chain(const ChainArgs &a, const ChainDims &m, cudaStream_t st);
+
 }  // namespace lfmmi

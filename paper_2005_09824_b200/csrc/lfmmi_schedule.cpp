@@ -19,6 +19,7 @@
 #include "lfmmi_schedule.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 namespace lfmmi {
@@ -51,6 +52,7 @@ GatherLayout make_gather_layout(int max_states, int num_pdfs) {
   auto round32 = [](int x) { return (x + 31) & ~31; };
   gl.r_stride = round32(max_states) + 16;  // copy 1 sits 16 banks over
   gl.rep_r = (2 * gl.r_stride <= 16383) ? 2 : 1;
+  if (const char *e = std::getenv("LFMMI_REP_R")) gl.rep_r = std::max(1, std::min(gl.rep_r, std::atoi(e)));
   if (gl.rep_r == 1) gl.r_stride = (max_states + 3) & ~3;
   gl.e_stride = round32(num_pdfs) + 8;  // copies shift by 8 banks
   gl.rep_e = 4;
@@ -209,6 +211,36 @@ void assign_xslots(const TileSchedule &tb, const int *pdf_of_arc, int num_pdfs, 
       }
     }
   }
+}
+
+void warp_lists(const std::vector<int> &trips, const std::vector<int> &bias,
+                std::vector<int> &table, std::vector<int> &list) {
+  const int nw = kTableNW, nt = int(trips.size());
+  std::vector<int> order(nt);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return trips[x] > trips[y]; });
+  std::vector<long> load(nw, 0);
+  for (int w = 0; w < nw; ++w) load[w] = w < int(bias.size()) ? bias[w] : 0;
+  std::vector<std::vector<int>> per(nw);
+  for (int t : order) {
+    int best = 0;
+    for (int w = 1; w < nw; ++w)
+      if (load[w] < load[best]) best = w;
+    per[best].push_back(t);
+    load[best] += trips[t];
+  }
+  table.assign(kWarpTable, 0);
+  list.clear();
+  for (int w = 0; w < nw; ++w) {
+    table[w] = int(list.size());
+    list.insert(list.end(), per[w].begin(), per[w].end());
+  }
+  table[nw] = int(list.size());
+  std::vector<int> by_load(nw);
+  std::iota(by_load.begin(), by_load.end(), 0);
+  std::stable_sort(by_load.begin(), by_load.end(),
+                   [&](int x, int y) { return load[x] < load[y]; });
+  for (int w = 0; w < nw; ++w) table[nw + 1 + w] = by_load[w];
 }
 
 }  // namespace lfmmi

@@ -34,4 +34,16 @@ void assign_xslots(const TileSchedule &tb, const int *pdf_of_arc, int num_pdfs, 
                    int slack, std::vector<int> &pdf_ptr, std::vector<int> &xslot_of_slot,
                    int &xpad);
 
+// Longest-processing-time assignment of the tiles of one phase to the NW
+// warps of a CTA-per-utterance kernel (kWarpTable ints per row and phase):
+//   table[0..NW]        per-warp ranges into `list` (CSR),
+//   table[NW+1..2NW]    warps in ascending final load (numerator tiles go to
+//                       the lightest warps first),
+// list: tile ids grouped by warp, each warp's tiles in descending trips.
+// `bias[w]` is the extra per-frame work warp w already carries (chores).
+constexpr int kTableNW = 16;
+constexpr int kWarpTable = 36;
+void warp_lists(const std::vector<int> &trips, const std::vector<int> &bias,
+                std::vector<int> &table, std::vector<int> &list);
+
 }  // namespace lfmmi

@@ -226,6 +226,7 @@ void posterior_kernel(int64_t h, torch::Tensor row_map, torch::Tensor expl, torc
 }
 
 std::string version() { return lfmmi_version(); }
+int64_t last_launch_count() { return lfmmi_last_launch_count(); }
 
 PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("graphs_create", &graphs_create);
@@ -238,4 +239,5 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("backward_kernel", &backward_kernel);
   m.def("posterior_kernel", &posterior_kernel);
   m.def("version", &version);
+  m.def("last_launch_count", &last_launch_count);
 }

@@ -116,10 +116,14 @@ def test_three_phase_api(cuda, name):
 
 
 # ------------------------------------------------- BASELINE configs vs oracle
-@pytest.mark.parametrize("kernel", ["auto", "group"])
+@pytest.mark.parametrize("kernel", ["auto", "fused", "fused1x", "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
                                                ("wsj_biphone", 4), ("sweep", 6)])
 def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
+    if kernel in ("fused", "fused1x"):  # single-launch num+den+grad kernel (opt-in)
+        monkeypatch.setenv("LFMMI_FUSED", "1")
+    if kernel == "fused1x":  # ... with a single posterior slot buffer
+        monkeypatch.setenv("LFMMI_CHAIN_SINGLE_X", "1")
     if kernel == "group":  # force the generic group kernel for the denominator
         monkeypatch.setenv("LFMMI_DISABLE_TILE", "1")
     w = synth.make_workload(config, seed=3, batch_size=batch_size)
@@ -129,6 +133,23 @@ def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
     assert _rel(res.objective, ref.objective) <= FP32_OBJ_REL
     assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
     assert res.num_failed == ref.num_failed == 0
+
+
+def test_large_graph_l2_path_vs_oracle(cuda):
+    """Config 4 (20k states / 200k arcs / 2000 pdfs): the state vectors leave no
+    room for the on-chip alpha ring, so the denominator runs the L2-streamed
+    group kernel (alpha read back from the HBM trellis)."""
+    w = synth.make_workload("large", seed=3, batch_size=2)
+    batch, nums, den = w.build(P)
+    res = P.chain_loss(batch, nums, den)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    assert _rel(res.objective, ref.objective) <= FP32_OBJ_REL
+    assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
+    assert res.num_failed == ref.num_failed == 0
+    fb = P.forward_backward(batch, den)
+    rf = O.forward_backward(batch, den, leak=1e-5)
+    np.testing.assert_allclose(fb.log_probs, rf.log_probs, rtol=1e-6)
+    assert np.abs(fb.posteriors - rf.posteriors).max() <= FP32_GRAD_ABS
 
 
 # ------------------------------------------ size-independent properties (full C2)
@@ -251,6 +272,18 @@ def test_pdf_mismatch_raises(cuda):
     batch = P.make_batch([np.zeros((2, 2))])
     with pytest.raises(ValueError, match="pdf dimension"):
         P.chain_loss(batch, P.ChainGraphBatch.broadcast(loop, 1), P.ChainGraphBatch.broadcast(loop, 1))
+
+
+@pytest.mark.parametrize("num_group", ["32", "64", "128"])
+def test_numerator_group_sizes(cuda, num_group, monkeypatch):
+    """Numerator pass with 1, 2 or 4 warps per utterance (B < 2 x SMs default: 4)."""
+    monkeypatch.setenv("LFMMI_NUM_GROUP", num_group)
+    w = synth.make_workload("wsj_mono", seed=4, batch_size=6)
+    batch, nums, den = w.build(P)
+    res = P.chain_loss(batch, nums, den)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    assert _rel(res.objective, ref.objective) <= FP32_OBJ_REL
+    assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
 
 
 def test_chain_loss_exact_workspace_concurrent_repeat(cuda):
