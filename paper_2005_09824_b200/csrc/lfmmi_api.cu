@@ -269,6 +269,11 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
     const int rc = launch_tile<Real>(a, graphs, small, st);
     if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
   }
+  // Arc packs too large for shared memory: stream them from L2 (coalesced tiles).
+  if (!small && !std::getenv("LFMMI_DISABLE_STREAM")) {
+    const int rc = launch_stream<Real>(a, graphs, st);
+    if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
+  }
   return launch_group<Real>(a, small ? choose_group(graphs->max_states) : 1024, st);
 }
 
@@ -279,8 +284,9 @@ using namespace lfmmi;
 extern "C" size_t lfmmi_workspace_size(int32_t max_states, int64_t total_frames,
                                        int32_t precision) {
   const size_t es = precision == LFMMI_F64 ? 8 : 4;
-  return size_t(pad4(std::max(1, int(max_states)))) * size_t(std::max<int64_t>(total_frames, 1)) *
-             es + 256;
+  // Row stride round32(S): the stream kernel spills alpha in 32-state tile order.
+  const size_t stride = size_t((std::max(1, int(max_states)) + 31) & ~31);
+  return stride * size_t(std::max<int64_t>(total_frames, 1)) * es + 256;
 }
 
 static int check_common(const lfmmi_graphs *graphs, int32_t batch, int32_t max_frames,

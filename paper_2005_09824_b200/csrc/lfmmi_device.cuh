@@ -27,6 +27,13 @@ __device__ __forceinline__ T warp_max(T v) {
   return v;
 }
 
+// Sum of the first n (<= 32) entries of v, identical in every lane.
+template <typename T>
+__device__ __forceinline__ T lane_sum_n(const T *v, int n, int lane) {
+  T x = lane < n ? v[lane] : T(0);
+  return warp_sum(x);
+}
+
 template <typename Real>
 __device__ __forceinline__ const Real *pick(const float *f, const double *d);
 template <>

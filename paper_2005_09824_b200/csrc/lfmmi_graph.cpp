@@ -64,6 +64,8 @@ struct HostPack {
   std::vector<unsigned> tf_info, tb_info, tf_word, tb_word;
   std::vector<int> tf_trips, tf_base, tb_trips, tb_base, pdf_arc_ptr;
   std::vector<int> tf_wlist, tb_wlist, tf_wtab, tb_wtab;
+  std::vector<int> sf_info, sb_info, sf_trips, sf_base, sb_trips, sb_base;
+  std::vector<uint2> sf_wp, sb_wp;
   std::vector<float> tf_p32, tb_p32;
   std::vector<double> tf_p64, tb_p64;
   std::vector<unsigned short> tb_xslot;
@@ -105,6 +107,8 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   int max_chunks = 0, max_in = 0, max_out = 0;
   int max_tiles = 0, max_tf = 0, max_tb = 0, max_xpad = 0;
   bool all_tileable = true;
+  bool all_streamable = true;
+  int max_stiles = 0;
   for (int r = 0; r < num_rows; ++r) {
     const int S = int(row_num_states[r]);
     const int I = int(row_num_arcs[r]);
@@ -217,6 +221,68 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
     h.pdf_chunk_ptr.push_back(nchunks);
     d[kNumChunks] = nchunks;
     max_chunks = std::max(max_chunks, nchunks);
+
+    // ---- stream packs (fb_stream_kernel): graphs too large for the on-chip packs ----
+    d[kSTileOff] = int(h.sf_trips.size());
+    d[kSTiles] = 0;
+    d[kSfSlotOff] = int(h.sf_wp.size());
+    d[kSbSlotOff] = int(h.sb_wp.size());
+    const bool want_stream = S > 512 && S <= 32767 && num_pdfs <= 131071;
+    if (want_stream) {
+      const size_t a0 = size_t(d[kArcOff]);
+      const int *iptr = &h.in_ptr[h.in_ptr.size() - (S + 1)];
+      const int *optr = &h.out_ptr[h.out_ptr.size() - (S + 1)];
+      const int nt = (S + 31) / 32;
+      auto pack = [&](const int *ptr, const int *gidx, const int *pdf, const double *prob,
+                      std::vector<int> &info, std::vector<int> &trips, std::vector<int> &base,
+                      std::vector<uint2> &wp) {
+        std::vector<int> order(S);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+          return (ptr[x + 1] - ptr[x]) > (ptr[y + 1] - ptr[y]);
+        });
+        int b = 0;
+        for (int t = 0; t < nt; ++t) {
+          int tr = 0;
+          for (int l = 0; l < 32; ++l) {
+            const int k = 32 * t + l;
+            info.push_back(k < S ? order[k] : -1);
+            if (k < S) tr = std::max(tr, ptr[order[k] + 1] - ptr[order[k]]);
+          }
+          trips.push_back(tr);
+          base.push_back(b);
+          for (int j = 0; j < tr; ++j)
+            for (int l = 0; l < 32; ++l) {
+              const int k = 32 * t + l;
+              uint2 v{0u, 0u};
+              if (k < S) {
+                const int s = order[k];
+                if (j < ptr[s + 1] - ptr[s]) {
+                  const int a = ptr[s] + j;
+                  const float f = float(prob[a]);
+                  v.x = unsigned(gidx[a]) | (unsigned(pdf[a]) << 15);
+                  std::memcpy(&v.y, &f, 4);
+                }
+              }
+              wp.push_back(v);
+            }
+          b += 32 * tr;
+        }
+        while (trips.size() % 4) {  // 16-byte aligned per-row tile arrays
+          trips.push_back(0);
+          base.push_back(0);
+          for (int l = 0; l < 32; ++l) info.push_back(-1);
+        }
+      };
+      pack(iptr, &h.in_src[a0], &h.in_pdf[a0], &h.in_p64[a0], h.sf_info, h.sf_trips, h.sf_base,
+           h.sf_wp);
+      pack(optr, &h.out_dst[a0], &h.out_pdf[a0], &h.out_p64[a0], h.sb_info, h.sb_trips, h.sb_base,
+           h.sb_wp);
+      d[kSTiles] = nt;
+      max_stiles = std::max(max_stiles, nt);
+    } else {
+      all_streamable = false;
+    }
 
     // ---- tile packs (scheduled, 16-bit state / pdf / posterior-slot encoding) ----
     bool tileable = S <= 16383 && num_pdfs <= 16383 && I <= 65535 && mi < 65536 && mo < 65536;
@@ -337,6 +403,8 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   g->max_tf_slots = max_tf;
   g->max_tb_slots = max_tb;
   g->tileable = all_tileable;
+  g->streamable = all_streamable;
+  g->max_stiles = max_stiles;
   g->max_xpad = max_xpad;
   g->rep_r = gl.rep_r;
   g->r_stride = gl.r_stride;
@@ -372,6 +440,14 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   add(h.tf_info, &dv.tf_info);
   add(h.tb_info, &dv.tb_info);
   add(h.tf_trips, &dv.tf_trips);
+  add(h.sf_info, &dv.sf_info);
+  add(h.sb_info, &dv.sb_info);
+  add(h.sf_trips, &dv.sf_trips);
+  add(h.sf_base, &dv.sf_base);
+  add(h.sb_trips, &dv.sb_trips);
+  add(h.sb_base, &dv.sb_base);
+  add(h.sf_wp, &dv.sf_wp);
+  add(h.sb_wp, &dv.sb_wp);
   add(h.tf_wlist, &dv.tf_wlist);
   add(h.tb_wlist, &dv.tb_wlist);
   add(h.tf_wtab, &dv.tf_wtab);

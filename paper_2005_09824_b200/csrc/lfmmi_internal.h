@@ -34,7 +34,13 @@ enum DescField : int {
   kTileable = 17,    // 1 if indices fit the 16-bit tile encoding
   kXPad = 18,        // posterior slot count incl. per-pdf padding + dummy slot (multiple of 4)
   kWTabOff = 19,     // offset into the per-phase warp tables (kWarpTable ints per row)
-  kDescInts = 20
+  // stream packs (fb_stream_kernel, L2-resident graphs): 32-state tiles by degree,
+  // slots {index | pdf << 15, fp32 prob} read straight from global memory
+  kSTileOff = 20,    // offset into s*_info (x32) / s*_trips / s*_base
+  kSTiles = 21,      // tiles per phase (0 = no stream pack for this row)
+  kSfSlotOff = 22,   // forward (by destination) slot offset
+  kSbSlotOff = 23,   // backward (by source) slot offset
+  kDescInts = 24
 };
 
 // Device-side view of a packed graph batch (passed by value to kernels).
@@ -66,6 +72,9 @@ struct DevGraphs {
   const unsigned short *tb_xslot;     // posterior slot of each backward arc
   const int *pdf_arc_ptr;             // posterior slot range per pdf (16-byte aligned)
   const uint2 *tf_wp, *tb_wp;         // interleaved (word, fp32 prob bits) slots
+  const int *sf_info, *sb_info;       // stream packs: state per tile lane (-1 = none)
+  const int *sf_trips, *sf_base, *sb_trips, *sb_base;
+  const uint2 *sf_wp, *sb_wp;         // {index | pdf << 15, fp32 prob bits}
 };
 
 }  // namespace lfmmi
@@ -75,6 +84,8 @@ struct lfmmi_graphs {
   int32_t max_chunks = 0, max_in_deg = 0, max_out_deg = 0;
   int32_t max_tiles = 0, max_tf_slots = 0, max_tb_slots = 0, max_xpad = 0;
   bool tileable = false;
+  bool streamable = false;  // every row has a stream pack (fb_stream_kernel)
+  int32_t max_stiles = 0;
   int32_t rep_r = 1, r_stride = 0, rep_e = 1, e_stride = 0;  // gather-vector replication
   void *device_block = nullptr;
   size_t device_bytes = 0;

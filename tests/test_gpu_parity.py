@@ -118,7 +118,8 @@ def test_three_phase_api(cuda, name):
 # ------------------------------------------------- BASELINE configs vs oracle
 @pytest.mark.parametrize("kernel", ["auto", "fused", "fused1x", "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
-                                               ("wsj_biphone", 4), ("sweep", 6)])
+                                               ("wsj_biphone", 4), ("wsj_biphone", 100),
+                                               ("sweep", 6)])
 def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
     if kernel in ("fused", "fused1x"):  # single-launch num+den+grad kernel (opt-in)
         monkeypatch.setenv("LFMMI_FUSED", "1")
@@ -126,6 +127,7 @@ def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
         monkeypatch.setenv("LFMMI_CHAIN_SINGLE_X", "1")
     if kernel == "group":  # force the generic group kernel for the denominator
         monkeypatch.setenv("LFMMI_DISABLE_TILE", "1")
+        monkeypatch.setenv("LFMMI_DISABLE_STREAM", "1")
     w = synth.make_workload(config, seed=3, batch_size=batch_size)
     batch, nums, den = w.build(P)
     res = P.chain_loss(batch, nums, den)
@@ -135,10 +137,16 @@ def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
     assert res.num_failed == ref.num_failed == 0
 
 
-def test_large_graph_l2_path_vs_oracle(cuda):
-    """Config 4 (20k states / 200k arcs / 2000 pdfs): the state vectors leave no
-    room for the on-chip alpha ring, so the denominator runs the L2-streamed
-    group kernel (alpha read back from the HBM trellis)."""
+@pytest.mark.parametrize("kernel", ["stream", "stream1", "group"])
+def test_large_graph_l2_path_vs_oracle(cuda, kernel, monkeypatch):
+    """Config 4 (20k states / 200k arcs / 2000 pdfs): the arc packs do not fit in
+    shared memory.  "stream": coalesced 32-state tiles streamed from L2
+    (fb_stream_kernel); "group": the generic CSR kernel with alpha read back
+    from the HBM trellis."""
+    if kernel == "group":
+        monkeypatch.setenv("LFMMI_DISABLE_STREAM", "1")
+    if kernel == "stream1":  # one CTA per utterance instead of a 2-CTA cluster
+        monkeypatch.setenv("LFMMI_STREAM_CLUSTER", "1")
     w = synth.make_workload("large", seed=3, batch_size=2)
     batch, nums, den = w.build(P)
     res = P.chain_loss(batch, nums, den)
@@ -150,6 +158,10 @@ def test_large_graph_l2_path_vs_oracle(cuda):
     rf = O.forward_backward(batch, den, leak=1e-5)
     np.testing.assert_allclose(fb.log_probs, rf.log_probs, rtol=1e-6)
     assert np.abs(fb.posteriors - rf.posteriors).max() <= FP32_GRAD_ABS
+    # deterministic: fixed-point posterior bins make the sums order-independent
+    again = P.chain_loss(batch, nums, den)
+    assert again.objective == res.objective
+    np.testing.assert_array_equal(again.grad, res.grad)
 
 
 # ------------------------------------------ size-independent properties (full C2)
