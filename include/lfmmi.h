@@ -139,6 +139,21 @@ int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *num_row_map,
                      double *totals, void *stream);
 
 /*
+ * Native text-FST ingestion (host only; no GPU needed).  Format and error
+ * contract of fst_io.py:53-110 (arc "src dst label [weight]", label = pdf+1,
+ * final "state [weight]", weight = -ln p, '#' comments, states densely
+ * re-indexed by first appearance; errors carry 1-based line numbers in
+ * lfmmi_last_error()).  Call _size first, then _parse into caller arrays
+ * (num_arcs entries each; final_probs has num_states entries, 0 = not final).
+ * Replaces: fst_io.py:53 parse_fst_text.
+ */
+int lfmmi_fst_text_size(const char *text, size_t length, int32_t num_pdfs,
+                        int64_t *num_states, int64_t *num_arcs);
+int lfmmi_fst_text_parse(const char *text, size_t length, int32_t num_pdfs, int64_t num_states,
+                         int64_t num_arcs, uint32_t *src, uint32_t *dst, uint32_t *pdf,
+                         double *prob, double *final_probs);
+
+/*
  * Parity/debug seam mirroring the numba kernels argument-for-argument (f64,
  * caller-allocated outputs written in place, trellis layouts (B,T+1,S_max)).
  * `expl` is the shifted emission probability array (B,T,D) f64.
