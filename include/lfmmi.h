@@ -112,6 +112,21 @@ int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t *row_map, i
                            const int32_t *other_fail, double *log_probs, int32_t *fail_frames,
                            double *scale_logs, void *stream);
 
+/*
+ * Ragged ("packed") variant: loglikes / posteriors are (sum_b T_b, D) with item
+ * b's frames at rows [sum_{j<b} T_j, sum_{j<=b} T_j) — no padding, any length
+ * order (device-side batching; replaces the host
+ * make_batch sort + zero-pad, batching.py:52-97).  max_frames = max_b T_b.
+ */
+int lfmmi_forward_backward_packed(const lfmmi_graphs *graphs, const int64_t *row_map,
+                                  int32_t batch, int32_t max_frames, int32_t num_pdfs,
+                                  int32_t precision, const void *loglikes, const int32_t *lengths,
+                                  double leak, double scale_floor, const void *leak_pi,
+                                  int64_t total_frames, void *workspace, size_t workspace_bytes,
+                                  void *posteriors, int32_t post_mode, const int32_t *other_fail,
+                                  double *log_probs, int32_t *fail_frames, double *scale_logs,
+                                  void *stream);
+
 /* Workspace bytes for lfmmi_chain_loss (both trellises + numerator posteriors). */
 size_t lfmmi_chain_loss_workspace_size(const lfmmi_graphs *numerators,
                                        const lfmmi_graphs *denominator, int32_t batch,
@@ -152,6 +167,16 @@ int lfmmi_fst_text_size(const char *text, size_t length, int32_t num_pdfs,
 int lfmmi_fst_text_parse(const char *text, size_t length, int32_t num_pdfs, int64_t num_states,
                          int64_t num_arcs, uint32_t *src, uint32_t *dst, uint32_t *pdf,
                          double *prob, double *final_probs);
+
+/* Ragged variant of lfmmi_chain_loss (loglikes / grad are (sum_b T_b, D)). */
+int lfmmi_chain_loss_packed(const lfmmi_graphs *numerators, const int64_t *num_row_map,
+                            const lfmmi_graphs *denominator, const int64_t *den_row_map,
+                            int32_t batch, int32_t max_frames, int32_t num_pdfs, int32_t precision,
+                            const void *loglikes, const int32_t *lengths, double leak,
+                            double scale_floor, const void *num_leak_pi, const void *den_leak_pi,
+                            int64_t total_frames, void *workspace, size_t workspace_bytes,
+                            void *grad, double *num_log_probs, double *den_log_probs,
+                            int32_t *num_fail, int32_t *den_fail, double *totals, void *stream);
 
 /*
  * Parity/debug seam mirroring the numba kernels argument-for-argument (f64,

@@ -18,7 +18,8 @@ from .forward_backward import (FBOptions, FBResult, ForwardResult, backward, for
                                forward_backward, forward_backward_device, get_precision,
                                occupation_posteriors, set_precision)
 from .graph import ChainGraph, ChainGraphBatch, Transition, device_graphs
-from .loss import ChainFunction, ChainLoss, ChainLossResult, chain_loss, chain_loss_device
+from .loss import (ChainFunction, ChainLoss, ChainLossResult, chain_loss, chain_loss_device,
+                   chain_loss_packed)
 
 __version__ = "0.1.0"
 
@@ -39,7 +40,7 @@ def get_num_threads() -> int:
 __all__ = [
     "ChainFunction", "ChainGraph", "ChainGraphBatch", "ChainLoss", "ChainLossResult", "FBOptions",
     "FBResult", "ForwardResult", "LogLikBatch", "Transition", "backward", "chain_loss",
-    "chain_loss_device", "device_graphs", "forward", "forward_backward",
+    "chain_loss_device", "chain_loss_packed", "device_graphs", "forward", "forward_backward",
     "forward_backward_device", "get_num_threads", "get_precision", "make_batch",
     "occupation_posteriors", "set_num_threads", "set_precision", "unsort", "__version__",
 ]

@@ -221,7 +221,7 @@ template <typename Real>
 int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_max, int D,
               const void *L, const int *lengths, double leak, double floor, const void *leak_pi,
               void *work, size_t work_bytes, void *post, int mode, const int *other_fail,
-              double *logp, int *fail, double *scale_logs, cudaStream_t st) {
+              double *logp, int *fail, double *scale_logs, cudaStream_t st, bool packed) {
   FBArgs<Real> a{};
   a.g = graphs->dev;
   a.row_map = row_map;
@@ -247,6 +247,7 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
   a.fail = fail;
   a.scale_logs = scale_logs;
   a.I_pad = pad4(std::max(1, graphs->max_arcs));
+  a.packed = packed ? 1 : 0;
   if (std::is_same<Real, float>::value) {  // f32 tile slots address replicated vectors
     a.rep_r = graphs->rep_r;
     a.r_stride = graphs->r_stride;
@@ -302,7 +303,7 @@ static int check_common(const lfmmi_graphs *graphs, int32_t batch, int32_t max_f
   return LFMMI_OK;
 }
 
-extern "C" int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t *row_map,
+static int forward_backward_impl(const lfmmi_graphs *graphs, const int64_t *row_map,
                                       int32_t batch, int32_t max_frames, int32_t num_pdfs,
                                       int32_t precision, const void *loglikes,
                                       const int32_t *lengths, double leak, double scale_floor,
@@ -310,7 +311,7 @@ extern "C" int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t 
                                       size_t workspace_bytes, void *posteriors,
                                       int32_t post_mode, const int32_t *other_fail,
                                       double *log_probs, int32_t *fail_frames,
-                                      double *scale_logs, void *stream) {
+                                      double *scale_logs, void *stream, bool packed) {
   int rc = check_common(graphs, batch, max_frames, num_pdfs, precision);
   if (rc) return rc;
   if (!row_map || !loglikes || !lengths || !workspace || !posteriors || !log_probs || !fail_frames)
@@ -327,10 +328,32 @@ extern "C" int lfmmi_forward_backward(const lfmmi_graphs *graphs, const int64_t 
   if (precision == LFMMI_F64)
     return run_fused<double>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
                              scale_floor, leak_pi, workspace, workspace_bytes, posteriors,
-                             post_mode, other_fail, log_probs, fail_frames, scale_logs, st);
+                             post_mode, other_fail, log_probs, fail_frames, scale_logs, st,
+                             packed);
   return run_fused<float>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
                           scale_floor, leak_pi, workspace, workspace_bytes, posteriors, post_mode,
-                          other_fail, log_probs, fail_frames, scale_logs, st);
+                          other_fail, log_probs, fail_frames, scale_logs, st, packed);
+}
+
+
+#define LFMMI_FB_PARAMS                                                                         \
+  const lfmmi_graphs *graphs, const int64_t *row_map, int32_t batch, int32_t max_frames,      \
+      int32_t num_pdfs, int32_t precision, const void *loglikes, const int32_t *lengths,      \
+      double leak, double scale_floor, const void *leak_pi, int64_t total_frames,             \
+      void *workspace, size_t workspace_bytes, void *posteriors, int32_t post_mode,           \
+      const int32_t *other_fail, double *log_probs, int32_t *fail_frames, double *scale_logs, \
+      void *stream
+#define LFMMI_FB_ARGS                                                                        \
+  graphs, row_map, batch, max_frames, num_pdfs, precision, loglikes, lengths, leak,          \
+      scale_floor, leak_pi, total_frames, workspace, workspace_bytes, posteriors, post_mode, \
+      other_fail, log_probs, fail_frames, scale_logs, stream
+
+extern "C" int lfmmi_forward_backward(LFMMI_FB_PARAMS) {
+  return forward_backward_impl(LFMMI_FB_ARGS, false);
+}
+
+extern "C" int lfmmi_forward_backward_packed(LFMMI_FB_PARAMS) {
+  return forward_backward_impl(LFMMI_FB_ARGS, true);
 }
 
 // Bytes of workspace for lfmmi_chain_loss: both alpha trellises (the two
@@ -362,15 +385,20 @@ extern "C" size_t lfmmi_chain_loss_workspace_size(const lfmmi_graphs *numerators
 // grad = (ok ? grad + gamma_num : 0) over valid rows; padded rows were zeroed
 // by the denominator pass.  Float4-vectorised grid-stride loop.
 template <typename Real>
-__global__ void combine_kernel(int B, int T_max, int D, const int *lengths, const int *num_fail,
-                               const int *den_fail, const Real *__restrict__ gnum,
-                               Real *__restrict__ grad) {
+__global__ void combine_kernel(bool packed, int B, int T_max, int D, const int *lengths,
+                               const int *num_fail, const int *den_fail,
+                               const Real *__restrict__ gnum, Real *__restrict__ grad) {
   const size_t row_elems = size_t(T_max) * D;
   for (int b = blockIdx.y; b < B; b += gridDim.y) {
     const size_t n = size_t(lengths[b]) * D;
     const bool ok = num_fail[b] < 0 && den_fail[b] < 0;
-    Real *g = grad + size_t(b) * row_elems;
-    const Real *q = gnum + size_t(b) * row_elems;
+    size_t base = size_t(b) * row_elems;
+    if (packed) {  // ragged rows: item b starts at sum_{j<b} T_j
+      base = 0;
+      for (int j = 0; j < b; ++j) base += size_t(lengths[j]) * D;
+    }
+    Real *g = grad + base;
+    const Real *q = gnum + base;
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += size_t(gridDim.x) * blockDim.x)
       g[i] = ok ? g[i] + q[i] : Real(0);
@@ -399,7 +427,7 @@ AuxStream &aux_for_device() {
 
 extern "C" int32_t lfmmi_last_launch_count(void) { return g_launches; }
 
-extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *num_row_map,
+static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_row_map,
                                 const lfmmi_graphs *denominator, const int64_t *den_row_map,
                                 int32_t batch, int32_t max_frames, int32_t num_pdfs,
                                 int32_t precision, const void *loglikes, const int32_t *lengths,
@@ -408,7 +436,7 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
                                 size_t workspace_bytes, void *grad, double *num_log_probs,
                                 double *den_log_probs,
                                 int32_t *num_fail, int32_t *den_fail, double *totals,
-                                void *stream) {
+                                void *stream, bool packed) {
   if (!numerators || !denominator)
     return set_error(LFMMI_ERR_INVALID, "lfmmi_chain_loss: NULL graph handle");
   size_t den_off, num_off, gam_off;
@@ -469,6 +497,7 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
     c.den_fail = den_fail;
     c.totals = totals;
     c.counter = reinterpret_cast<unsigned *>(ws + gam_off);
+    c.packed = packed ? 1 : 0;
     ChainDims m{};
     m.Fd = std::max(denominator->max_tf_slots, denominator->max_tb_slots);
     m.ntd = denominator->max_tiles;
@@ -495,17 +524,17 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
   // claim whole SMs; the numerator warps fill the SMs it leaves free.
   rc = check_cuda(cudaEventRecord(ax.fork, st), "cudaEventRecord(fork)");
   if (rc) return rc;
-  rc = lfmmi_forward_backward(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
+  rc = forward_backward_impl(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
                               loglikes, lengths, leak, scale_floor, den_leak_pi, total_frames,
                               ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE, nullptr, den_log_probs,
-                              den_fail, nullptr, stream);
+                              den_fail, nullptr, stream, packed);
   if (rc) return rc;
   rc = check_cuda(cudaStreamWaitEvent(ax.aux, ax.fork, 0), "cudaStreamWaitEvent(fork)");
   if (rc) return rc;
-  rc = lfmmi_forward_backward(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
+  rc = forward_backward_impl(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
                               loglikes, lengths, leak, scale_floor, num_leak_pi, total_frames,
                               ws + num_off, num_bytes, ws + gam_off, LFMMI_POST_WRITE, nullptr, num_log_probs,
-                              num_fail, nullptr, nst);
+                              num_fail, nullptr, nst, packed);
   if (rc) return rc;
   rc = check_cuda(cudaEventRecord(ax.join, nst), "cudaEventRecord(join)");
   if (rc) return rc;
@@ -515,12 +544,12 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
     const dim3 grid(std::max(1, std::min(32, (max_frames * num_pdfs + 1023) / 1024)),
                     std::min(batch, 4096));
     if (precision == LFMMI_F64)
-      combine_kernel<double><<<grid, 256, 0, st>>>(batch, max_frames, num_pdfs, lengths, num_fail,
+      combine_kernel<double><<<grid, 256, 0, st>>>(packed, batch, max_frames, num_pdfs, lengths, num_fail,
                                                    den_fail,
                                                    reinterpret_cast<const double *>(ws + gam_off),
                                                    static_cast<double *>(grad));
     else
-      combine_kernel<float><<<grid, 256, 0, st>>>(batch, max_frames, num_pdfs, lengths, num_fail,
+      combine_kernel<float><<<grid, 256, 0, st>>>(packed, batch, max_frames, num_pdfs, lengths, num_fail,
                                                   den_fail,
                                                   reinterpret_cast<const float *>(ws + gam_off),
                                                   static_cast<float *>(grad));
@@ -534,6 +563,26 @@ extern "C" int lfmmi_chain_loss(const lfmmi_graphs *numerators, const int64_t *n
   }
   g_launches = rc == LFMMI_OK ? (totals ? 4 : 3) : 0;
   return rc;
+}
+
+
+#define LFMMI_CL_PARAMS                                                                        \
+  const lfmmi_graphs *numerators, const int64_t *num_row_map, const lfmmi_graphs *denominator, \
+      const int64_t *den_row_map, int32_t batch, int32_t max_frames, int32_t num_pdfs,         \
+      int32_t precision, const void *loglikes, const int32_t *lengths, double leak,            \
+      double scale_floor, const void *num_leak_pi, const void *den_leak_pi,                    \
+      int64_t total_frames, void *workspace, size_t workspace_bytes, void *grad,               \
+      double *num_log_probs, double *den_log_probs, int32_t *num_fail, int32_t *den_fail,      \
+      double *totals, void *stream
+#define LFMMI_CL_ARGS                                                                         \
+  numerators, num_row_map, denominator, den_row_map, batch, max_frames, num_pdfs, precision,  \
+      loglikes, lengths, leak, scale_floor, num_leak_pi, den_leak_pi, total_frames, workspace, \
+      workspace_bytes, grad, num_log_probs, den_log_probs, num_fail, den_fail, totals, stream
+
+extern "C" int lfmmi_chain_loss(LFMMI_CL_PARAMS) { return chain_loss_impl(LFMMI_CL_ARGS, false); }
+
+extern "C" int lfmmi_chain_loss_packed(LFMMI_CL_PARAMS) {
+  return chain_loss_impl(LFMMI_CL_ARGS, true);
 }
 
 extern "C" int lfmmi_forward_kernel(const lfmmi_graphs *graphs, const int64_t *row_map,

@@ -235,8 +235,13 @@ __global__ void __launch_bounds__(GROUP, 1)
   const float lam = a.leak;
   float *trd = a.trellis_d + item_off * a.Sd_pad;
   float *trn = a.trellis_n + item_off * a.Sn_pad;
+  if (a.packed) {  // ragged layout: item b's rows start at sum_{j<b} T_j
+    Lb = a.L + size_t(item_off) * D;
+    gb = a.grad + size_t(item_off) * D;
+  }
 
-  for (size_t i = tid; i < size_t(a.T_max - T) * D; i += GROUP) gb[size_t(T) * D + i] = 0.f;
+  if (!a.packed)
+    for (size_t i = tid; i < size_t(a.T_max - T) * D; i += GROUP) gb[size_t(T) * D + i] = 0.f;
 
   auto issue_row = [&](int t) {
     if (t < 0 || t >= T || cwarp >= nrw || skip(6)) return;

@@ -85,6 +85,7 @@ struct FBArgs {
   double *scale_logs;
   int I_pad;  // tile kernel: per-arc scratch (posterior slots)
   int rep_r, r_stride, rep_e, e_stride;  // tile kernel: gather-vector replication
+  int packed;  // 1: L / posteriors are ragged (sum_b T_b, D), item b at row sum_{j<b} T_j
 };
 
 }  // namespace lfmmi

@@ -143,8 +143,12 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
   const Real pisum = pi ? Real(pisum_d) : Real(1);
   const Real lam = a.leak;
   Real *trellis = a.work + item_off * S_pad;
+  if (a.packed) {  // ragged layout: item b's rows start at sum_{j<b} T_j
+    Lb = a.L + size_t(item_off) * D;
+    post_b = a.post + size_t(item_off) * D;
+  }
 
-  if (!reads_post) {
+  if (!reads_post && !a.packed) {
     const size_t n = size_t(a.T_max - T) * D;
     for (size_t i = tid; i < n; i += GROUP) post_b[size_t(T) * D + i] = Real(0);
   }

@@ -46,6 +46,7 @@ struct ChainArgs {
   unsigned *counter;
   long long *prof;  // debug section timers (LFMMI_PROFILE), normally NULL
   int ablate;       // debug ablation bits (LFMMI_ABLATE, profiled launches only)
+  int packed;       // ragged (sum_b T_b, D) loglikes / grad
 };
 
 struct ChainDims {

@@ -147,10 +147,15 @@ __global__ void __launch_bounds__(NT, 1)
   long long item_off = 0;
   for (int w = 0; w < NW; ++w) item_off += lscr[w];
   float *trellis = a.work + item_off * S32;  // rows in backward-pack state order
+  if (a.packed) {  // ragged layout: item b's rows start at sum_{j<b} T_j
+    Lb = a.L + size_t(item_off) * D;
+    post_b = a.post + size_t(item_off) * D;
+  }
   const float upi = float(1.0 / double(S));
   const float lam = a.leak;
 
-  for (size_t i = tid; i < size_t(a.T_max - T) * D; i += NT) post_b[size_t(T) * D + i] = 0.f;
+  if (!a.packed)
+    for (size_t i = tid; i < size_t(a.T_max - T) * D; i += NT) post_b[size_t(T) * D + i] = 0.f;
 
   // ---- log-likelihood rows in registers (two frames ahead) ----------------------
   float rn[kEPT], rn2[kEPT];

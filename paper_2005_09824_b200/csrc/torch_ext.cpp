@@ -167,6 +167,36 @@ void chain_loss(int64_t num_h, torch::Tensor num_row_map, int64_t den_h, torch::
         "lfmmi_chain_loss");
 }
 
+// Ragged input: loglikes (sum_b T_b, D), item b at rows [sum_{j<b} T_j, ...).
+void chain_loss_packed(int64_t num_h, torch::Tensor num_row_map, int64_t den_h,
+                       torch::Tensor den_row_map, torch::Tensor loglikes, torch::Tensor lengths,
+                       int64_t max_frames, double leak, double scale_floor, int64_t total_frames,
+                       torch::Tensor workspace, torch::Tensor grad, torch::Tensor num_log_probs,
+                       torch::Tensor den_log_probs, torch::Tensor num_fail, torch::Tensor den_fail,
+                       torch::Tensor totals) {
+  const c10::cuda::CUDAGuard guard(loglikes.device());
+  const auto dt = loglikes.scalar_type();
+  need_cuda(num_row_map, torch::kInt64, "num_row_map");
+  need_cuda(den_row_map, torch::kInt64, "den_row_map");
+  need_cuda(loglikes, dt, "loglikes");
+  need_cuda(lengths, torch::kInt32, "lengths");
+  need_cuda(workspace, torch::kUInt8, "workspace");
+  need_cuda(grad, dt, "grad");
+  need_cuda(totals, torch::kFloat64, "totals");
+  TORCH_CHECK(loglikes.dim() == 2, "packed loglikes must be (sum T, D)");
+  TORCH_CHECK(grad.sizes() == loglikes.sizes(), "grad must match loglikes");
+  check(lfmmi_chain_loss_packed(
+            as_graphs(num_h), num_row_map.data_ptr<int64_t>(), as_graphs(den_h),
+            den_row_map.data_ptr<int64_t>(), int32_t(lengths.size(0)), int32_t(max_frames),
+            int32_t(loglikes.size(1)), precision_of(loglikes), loglikes.data_ptr(),
+            lengths.data_ptr<int32_t>(), leak, scale_floor, nullptr, nullptr, total_frames,
+            workspace.data_ptr(), size_t(workspace.numel()), grad.data_ptr(),
+            num_log_probs.data_ptr<double>(), den_log_probs.data_ptr<double>(),
+            num_fail.data_ptr<int32_t>(), den_fail.data_ptr<int32_t>(), totals.data_ptr<double>(),
+            stream_of(loglikes)),
+        "lfmmi_chain_loss_packed");
+}
+
 void forward_kernel(int64_t h, torch::Tensor row_map, torch::Tensor expl, torch::Tensor lengths,
                     double leak, torch::Tensor leak_pi, double scale_floor, torch::Tensor alpha,
                     torch::Tensor scales, torch::Tensor fail_frames) {
@@ -235,6 +265,7 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("chain_loss_workspace_size", &chain_loss_workspace_size);
   m.def("forward_backward", &forward_backward);
   m.def("chain_loss", &chain_loss);
+  m.def("chain_loss_packed", &chain_loss_packed);
   m.def("forward_kernel", &forward_kernel);
   m.def("backward_kernel", &backward_kernel);
   m.def("posterior_kernel", &posterior_kernel);

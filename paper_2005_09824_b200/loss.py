@@ -25,7 +25,8 @@ from .forward_backward import (FBOptions, _check_compatible, _dtype, _leak_distr
                                _to_device, _workspace)
 from .graph import ChainGraphBatch, device_graphs
 
-__all__ = ["ChainLossResult", "chain_loss", "chain_loss_device", "ChainFunction", "ChainLoss"]
+__all__ = ["ChainLossResult", "chain_loss", "chain_loss_device", "chain_loss_packed",
+           "ChainFunction", "ChainLoss"]
 
 
 @dataclass
@@ -78,6 +79,55 @@ def chain_loss_device(values, lengths, numerators, denominator, opts: FBOptions 
     return grad, num_lp, den_lp, num_fail, den_fail, totals
 
 
+def chain_loss_packed(values, lengths, numerators, denominator, opts: FBOptions = FBOptions(), *,
+                      max_frames: int | None = None, total_frames: int | None = None, grad=None):
+    """LF-MMI on a ragged (packed) batch — device-side batching.
+
+    ``values`` (sum_b T_b, D) CUDA float32/float64 with utterance b's frames at
+    rows ``[sum_{j<b} T_j, sum_{j<=b} T_j)``; ``lengths`` (B,) CUDA int32, any
+    order (no host sort, no padding: replaces make_batch, batching.py:52-97);
+    ``numerators`` aligned with ``lengths``.  Returns the same tuple as
+    :func:`chain_loss_device` with ``grad`` in the packed layout (caller order).
+    Uniform leak distribution.  ``max_frames`` / ``total_frames`` default to a
+    host read of ``lengths``.
+    """
+    import torch
+
+    ext = _backend.require_cuda()
+    dev = values.device
+    if values.dim() != 2:
+        raise ValueError(f"packed values must be (sum T, D), got {tuple(values.shape)}")
+    if opts.leak_distribution is not None:
+        raise ValueError("chain_loss_packed supports the uniform leak distribution only")
+    B = int(lengths.shape[0])
+    N, D = values.shape
+    if max_frames is None or total_frames is None:
+        lens = lengths.cpu()
+        max_frames = int(lens.max()) if max_frames is None else max_frames
+        total_frames = int(lens.sum()) if total_frames is None else total_frames
+    if total_frames != N:
+        raise ValueError(f"sum of lengths {total_frames} != packed rows {N}")
+    ng = device_graphs(_as_graph_batch(numerators, B), dev)
+    dgr = device_graphs(_as_graph_batch(denominator, B), dev)
+    if ng.num_pdfs != D or dgr.num_pdfs != D:
+        raise ValueError(f"pdf dimension mismatch: values have {D}, graphs have "
+                         f"{ng.num_pdfs}/{dgr.num_pdfs}")
+    prec = 1 if values.dtype == torch.float64 else 0
+    ws = _workspace(dev, ext.chain_loss_workspace_size(ng.handle, dgr.handle, B, int(max_frames),
+                                                       int(D), int(total_frames), prec))
+    if grad is None:
+        grad = torch.empty_like(values)
+    f64 = dict(dtype=torch.float64, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    num_lp, den_lp = torch.empty(B, **f64), torch.empty(B, **f64)
+    num_fail, den_fail = torch.empty(B, **i32), torch.empty(B, **i32)
+    totals = torch.empty(3, **f64)
+    ext.chain_loss_packed(ng.handle, ng.row_map, dgr.handle, dgr.row_map, values, lengths,
+                          int(max_frames), float(opts.leak_coefficient), float(opts.scale_floor),
+                          int(total_frames), ws, grad, num_lp, den_lp, num_fail, den_fail, totals)
+    return grad, num_lp, den_lp, num_fail, den_fail, totals
+
+
 def chain_loss(batch, numerators, denominator, opts: FBOptions = FBOptions(),
                normalize_by_frames: bool = True, precision: str | None = None) -> ChainLossResult:
     """MMI objective and gradient for one batch (loss.py:42-84), computed on the GPU."""
@@ -121,8 +171,9 @@ def _autograd_function():
         ``apply(input, input_lengths, numerators, denominator, opts,
         normalize_by_frames, process_group)`` -> scalar loss
         ``-sum_ok(logP_num - logP_den) / frames`` (or un-normalised).
-        ``input`` is (B, T, D) on CUDA in any length order; ``numerators`` is
-        aligned with it.  Backward returns ``-(gamma_num - gamma_den) / frames``
+        ``input`` is (B, T, D) on CUDA in any length order — or ragged
+        (sum_b T_b, D) with ``input_lengths`` giving the split; ``numerators``
+        is aligned with it.  Backward returns ``-(gamma_num - gamma_den) / frames``
         scaled by the incoming gradient.
         """
 
@@ -135,10 +186,13 @@ def _autograd_function():
             if x.dtype not in (torch.float32, torch.float64):
                 x = x.float()
             lengths = input_lengths.to(device=x.device, dtype=torch.int32).contiguous()
-            B = x.shape[0]
+            B = lengths.shape[0]
             nums = _as_graph_batch(numerators, B)
             den = _as_graph_batch(denominator, B)
-            grad, _, _, _, _, totals = chain_loss_device(x, lengths, nums, den, opts)
+            if x.dim() == 2:  # ragged (sum T, D) input: device-side batching
+                grad, _, _, _, _, totals = chain_loss_packed(x, lengths, nums, den, opts)
+            else:
+                grad, _, _, _, _, totals = chain_loss_device(x, lengths, nums, den, opts)
             if process_group is not None:
                 import torch.distributed as dist
 

@@ -298,6 +298,58 @@ def test_numerator_group_sizes(cuda, num_group, monkeypatch):
     assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
 
 
+@pytest.mark.parametrize("kernel", ["auto", "fused", "stream"])
+@pytest.mark.parametrize("config,batch_size", [("wsj_mono", 7), ("sweep", 5),
+                                               ("wsj_biphone", 3), ("large", 2)])
+def test_packed_ragged_batch_any_order(cuda, config, batch_size, kernel, monkeypatch):
+    """Device-side batching: (sum T, D) ragged input in caller (unsorted) order,
+    no padding; grad comes back in the same ragged layout."""
+    import torch
+
+    if kernel == "fused":
+        monkeypatch.setenv("LFMMI_FUSED", "1")
+    if kernel == "stream" and config not in ("wsj_biphone", "large"):
+        pytest.skip("stream kernel is for graphs beyond shared memory")
+    w = synth.make_workload(config, seed=6, batch_size=batch_size)
+    batch, nums, den = w.build(P)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    order = np.random.default_rng(0).permutation(batch.batch_size)  # arbitrary caller order
+    seqs = [batch.values[b, :batch.lengths[b]] for b in order]
+    dev = torch.device("cuda", 0)
+    x = torch.tensor(np.concatenate(seqs), dtype=torch.float32, device=dev)
+    lens = torch.tensor([len(q) for q in seqs], dtype=torch.int32, device=dev)
+    num_list = [nums.graph(int(b)) for b in order]
+    g, nl, dl, nf, df, tot = P.chain_loss_packed(x, lens, num_list, den.graph(0))
+    tot = tot.cpu().numpy()
+    assert _rel(float(tot[0]), ref.objective) <= FP32_OBJ_REL
+    assert int(round(tot[1])) == int(batch.lengths.sum()) and int(round(tot[2])) == 0
+    g = g.double().cpu().numpy()
+    offs = np.concatenate([[0], np.cumsum([len(q) for q in seqs])])
+    for k, b in enumerate(order):
+        assert np.abs(g[offs[k]:offs[k + 1]] - ref.grad[b, :batch.lengths[b]]).max() <= FP32_GRAD_ABS
+    nl = nl.cpu().numpy()
+    for k, b in enumerate(order):
+        assert _rel(nl[k], ref.per_utt[b][0]) <= 1e-5
+
+
+def test_chain_function_packed_input(cuda):
+    import torch
+
+    w = synth.make_workload("wsj_mono", seed=8, batch_size=4)
+    batch, nums, den = w.build(P)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    x = torch.tensor(np.concatenate([batch.values[b, :batch.lengths[b]] for b in range(4)]),
+                     dtype=torch.float32, device="cuda", requires_grad=True)
+    lens = torch.tensor(batch.lengths, dtype=torch.int32)
+    loss = P.ChainFunction.apply(x, lens, nums, den)
+    loss.backward()
+    assert _rel(float(loss.detach()), ref.loss) <= 1e-5
+    frames = int(batch.lengths.sum())
+    g = x.grad.double().cpu().numpy()
+    exp = np.concatenate([-ref.grad[b, :batch.lengths[b]] / frames for b in range(4)])
+    assert np.abs(g - exp).max() <= FP32_GRAD_ABS
+
+
 def test_chain_loss_exact_workspace_concurrent_repeat(cuda):
     """Regression: numerator and denominator passes run concurrently and share one
     exactly-sized workspace; repeated calls must not overlap their regions."""
