@@ -319,7 +319,10 @@ def run_ours(args):
     peak = peak or 6650.0
     achieved = A / (kernel_ms / 1e3) / 1e9
     ncu = load_json(NCU_SUMMARY) or {}
-    traffic = ncu.get("chain_dram_bytes_per_launch" if fused else "den_dram_bytes_per_launch")
+    # ncu traffic is recorded for the headline workload only (profiles/ncu_summary.json)
+    traffic = None
+    if ncu.get("workload", "wsj_mono") == args.config and args.batch is None:
+        traffic = ncu.get("chain_dram_bytes_per_launch" if fused else "den_dram_bytes_per_launch")
 
     # ---- end-to-end through the public API with host buffers ----------------
     e2e = None

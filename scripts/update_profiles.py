@@ -44,8 +44,8 @@ def main(tag):
             w.writerow(["id", "kernel", "gpu__time_duration.sum_ns"])
             for r in rows[start + 1:]:
                 w.writerow([r[iid], r[kn][:110], r[mv]])
-    summ = {"round": tag, "source": "ncu --set full --clock-control none; bench.py --profile "
-                                    "(wsj_mono, seed 0)"}
+    summ = {"round": tag, "workload": "wsj_mono",
+            "source": "ncu --set full --clock-control none; bench.py --profile (wsj_mono, seed 0)"}
     txt = []
     for name in ("den", "num", "chain"):
         rep = os.path.join(G, f"prof_{name}.ncu-rep")
