@@ -411,8 +411,10 @@ struct AuxStream {
   cudaStream_t aux = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
+// One auxiliary stream + fork/join events per (host thread, device): concurrent
+// lfmmi_chain_loss calls from different threads never share event objects.
 AuxStream &aux_for_device() {
-  static AuxStream per_dev[64];
+  static thread_local AuxStream per_dev[64];
   int dev = 0;
   cudaGetDevice(&dev);
   AuxStream &a = per_dev[dev & 63];

@@ -152,9 +152,11 @@ _WORKSPACE: dict = {}
 
 
 def _workspace(device, nbytes: int):
+    """Scratch for one call, cached per (device, current stream): calls queued on
+    one stream reuse it safely; calls on different streams never share it."""
     import torch
 
-    key = (device.index, )
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
     buf = _WORKSPACE.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)

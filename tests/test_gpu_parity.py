@@ -350,6 +350,28 @@ def test_chain_function_packed_input(cuda):
     assert np.abs(g - exp).max() <= FP32_GRAD_ABS
 
 
+def test_concurrent_streams_do_not_share_scratch(cuda):
+    """Two batches on two CUDA streams at once: per-stream workspaces and
+    per-thread auxiliary streams keep them independent."""
+    import torch
+
+    outs = []
+    ws = [synth.make_workload("wsj_mono", seed=s, batch_size=6) for s in (11, 12)]
+    built = [w.build(P) for w in ws]
+    refs = [O.chain_loss(*b, leak=1e-5) for b in built]
+    streams = [torch.cuda.Stream() for _ in built]
+    tensors = [(torch.tensor(b[0].values, dtype=torch.float32, device="cuda"),
+                torch.tensor(b[0].lengths, dtype=torch.int32, device="cuda")) for b in built]
+    torch.cuda.synchronize()
+    for (x, l), b, st in zip(tensors, built, streams):
+        with torch.cuda.stream(st):
+            outs.append(P.chain_loss_device(x, l, b[1], b[2]))
+    torch.cuda.synchronize()
+    for o, ref in zip(outs, refs):
+        assert _rel(float(o[5][0].item()), ref.objective) <= FP32_OBJ_REL
+        assert np.abs(o[0].double().cpu().numpy() - ref.grad).max() <= FP32_GRAD_ABS
+
+
 def test_chain_loss_exact_workspace_concurrent_repeat(cuda):
     """Regression: numerator and denominator passes run concurrently and share one
     exactly-sized workspace; repeated calls must not overlap their regions."""
