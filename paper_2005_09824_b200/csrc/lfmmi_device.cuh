@@ -42,6 +42,9 @@ template <>
 __device__ __forceinline__ const double *pick<double>(const float *, const double *d) { return d; }
 
 __device__ __forceinline__ float exp_r(float x) { return expf(x); }
+// Correctly rounded reciprocal (== 1 / x in IEEE round-to-nearest), no division subroutine.
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
 __device__ __forceinline__ double exp_r(double x) { return exp(x); }
 
 // ---- cp.async (LDGSTS) -----------------------------------------------------

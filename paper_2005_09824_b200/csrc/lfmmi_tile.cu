@@ -261,8 +261,12 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   };
 
   // alpha/beta columns are replicated (rep_r copies, see lfmmi_schedule.cpp)
+  // (rep_r is 1 or 2, make_gather_layout; hoisted so no per-store param reloads)
+  const bool rep2 = a.rep_r > 1;
+  const int rstride = a.r_stride;
   auto put_vec = [&](Real *v, int s, Real x) {
-    for (int c = 0; c < a.rep_r; ++c) v[c * a.r_stride + s] = x;
+    v[s] = x;
+    if (rep2) v[rstride + s] = x;
   };
   // ---- prologue -----------------------------------------------------------------
   for (int s = tid; s < S; s += GROUP) put_vec(rbuf, s, (s == init) ? Real(1) : Real(0));
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
         fail_at = k - 1;
         break;
       }
-      inv2 = Real(1) / t2;
+      inv2 = rcp_rn(t2);
       if (tid == 0) scales[k - 1] = t2;
     }
     {
@@ -436,15 +440,18 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   };
   // gamma_t[d] = sum of pdf d's slots: SPL chore lanes per pdf, each summing
   // float4 groups, combined by a shuffle within the SPL-lane segment.
-  int spl = 1;
-  while (spl < 32 && D * spl * 2 <= GROUP) spl <<= 1;
+  int spl = 1, spl_log = 0;  // lanes per pdf in the flush (power of two)
+  while (spl < 32 && D * spl * 2 <= GROUP) {
+    spl <<= 1;
+    ++spl_log;
+  }
   auto flush_post = [&](int t) {
     Real *prow = post_b + size_t(t) * D;
     const Real *old = gstage + (t & 1) * D_pad;
     const int sub = ctid & (spl - 1);
     for (int base_i = 0; base_i < D * spl; base_i += GROUP) {
       const int idx = base_i + ctid;
-      const int d = idx / spl;
+      const int d = idx >> spl_log;
       Real g = Real(0);
       if (d < D) {
         const int lo = pdfptr[d] >> 2, hi = pdfptr[d + 1] >> 2;
@@ -478,7 +485,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     const int ct = t & 1, cp = ct ^ 1;
     Real ld = Real(0);
     if (t < T && lam > Real(0)) ld = lam * lane_sum<NW>(part + ct * 32, lane);
-    const Real inv = Real(1) / scales[t - 1];
+    const Real inv = rcp_rn(scales[t - 1]);
     if (t - 2 >= 0) compute_e(t - 2, false);
     issue_row(t - 3);
     issue_alpha(t - 2);

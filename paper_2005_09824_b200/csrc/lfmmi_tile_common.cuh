@@ -120,7 +120,19 @@ __device__ __forceinline__ void fwd_tile_f32(uint32_t sb, int trips, uint32_t e3
     A = fmaf(q3, r3, A);
     if (LEAKY) Bs += (q0 + q1) + (q2 + q3);
   }
-  for (; j < trips; ++j, sb += 256) {
+  // Remainder (trips % 4 rows) without a loop: at most one pair and one single.
+  if (j + 2 <= trips) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
+    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu));
+    const float q0 = __uint_as_float(w0.y) * e0, q1 = __uint_as_float(w1.y) * e1;
+    A = fmaf(q0, r0, A);
+    A = fmaf(q1, r1, A);
+    if (LEAKY) Bs += q0 + q1;
+    j += 2;
+    sb += 2 * 256;
+  }
+  if (j < trips) {
     const uint2 w = lds_v2(sb);
     const float q = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16));
     A = fmaf(q, lds_f(r32 + (w.x & 0xFFFFu)), A);
@@ -153,7 +165,21 @@ __device__ __forceinline__ float bwd_tile_f32(uint32_t sb, uint32_t xb, int trip
     sts_f(x32 + 4 * x2, as * t2);
     sts_f(x32 + 4 * x3, as * t3);
   }
-  for (; j < trips; ++j, sb += 256, xb += 64) {
+  if (j + 2 <= trips) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
+    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
+    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu));
+    const float t0 = __uint_as_float(w0.y) * e0 * (b0 + ld),
+                t1 = __uint_as_float(w1.y) * e1 * (b1 + ld);
+    A += t0 + t1;
+    sts_f(x32 + 4 * x0, as * t0);
+    sts_f(x32 + 4 * x1, as * t1);
+    j += 2;
+    sb += 2 * 256;
+    xb += 2 * 64;
+  }
+  if (j < trips) {
     const uint2 w = lds_v2(sb);
     const uint32_t x = lds_h(xb);
     const float t = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16)) *
