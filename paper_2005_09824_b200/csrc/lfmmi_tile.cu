@@ -32,7 +32,9 @@
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
 #include "lfmmi_tile_common.cuh"
+#include "lfmmi_schedule.h"
 
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -40,13 +42,13 @@
 namespace lfmmi {
 
 struct TileLayout {  // byte offsets of one utterance's slice of shared memory
-  size_t wp, xs, tinfo, ttrips, tbase, pdfptr, xterm, rbuf, aring, ebuf, stage, gstage, scales,
-      shifts, part, mpart, total;
+  size_t wp, xs, tinfo, ttrips, tbase, wlist, wtab, pdfptr, xterm, rbuf, aring, ebuf, stage,
+      gstage, scales, shifts, part, mpart, total;
 };
 
 __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int ntiles, int D,
                                                   int X_pad, int S_pad, int D_pad, int T_pad,
-                                                  int RB, int EB, int real) {
+                                                  int RB, int EB, int real, int nx = 1) {
   TileLayout l;
   size_t o = 512;  // scratch: 32 doubles + 32 int64
   const size_t F = smem_graph ? size_t(Fmax) : 0;
@@ -56,8 +58,10 @@ __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int
   l.tinfo = o;   o = al16(o + nt * 32 * 4);
   l.ttrips = o;  o = al16(o + size_t(pad4(int(nt))) * 4);
   l.tbase = o;   o = al16(o + size_t(pad4(int(nt))) * 4);
+  l.wlist = o;   o = al16(o + (nx > 1 ? size_t(pad4(int(nt))) * 4 + kWarpTable * 4 : 0));
+  l.wtab = l.wlist + (nx > 1 ? size_t(pad4(int(nt))) * 4 : 0);
   l.pdfptr = o;  o = al16(o + size_t(D + 1) * 4);
-  l.xterm = o;   o = al16(o + size_t(X_pad) * real);      // posterior slots (one frame)
+  l.xterm = o;   o = al16(o + size_t(nx) * X_pad * real); // posterior slots (nx frames)
   l.rbuf = o;    o = al16(o + size_t(2) * RB * real);     // alpha/beta columns x copies
   l.aring = o;   o = al16(o + size_t(2) * S_pad * real);
   l.ebuf = o;    o = al16(o + size_t(2) * EB * real);     // emission rows x copies
@@ -81,9 +85,16 @@ __device__ __forceinline__ void tsync() {
   }
 }
 
-template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI>
+// XDB (denominator, fp32, when shared memory allows): two posterior slot
+// buffers, so the gradient row of frame t is flushed by the top warps at the
+// start of the next backward iteration — overlapped with the other warps' arc
+// work — instead of between two extra barriers; tiles then follow the host's
+// LPT warp lists, which give the flushing warps fewer arcs.
+template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI, bool XDB = false>
 __global__ void __launch_bounds__(GROUP *IPC, 1)
     fb_tile_kernel(const FBArgs<Real> a, int Fmax, int ntiles_max, int X_pad) {
+  static_assert(!XDB || (GROUP == 32 * kTableNW && IPC == 1 && SMEM_GRAPH),
+                "XDB uses the 16-warp LPT lists");
   constexpr int NW = GROUP / 32;
   using Slot = typename SlotOf<Real>::type;
   extern __shared__ __align__(16) unsigned char smem_all[];
@@ -98,7 +109,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   if (b >= a.B) return;  // whole group exits together (no CTA-wide barriers for IPC > 1)
   const int RB = a.rep_r * a.r_stride, EB = a.rep_e * a.e_stride;
   const TileLayout lay = tile_layout(SMEM_GRAPH, Fmax, ntiles_max, a.D, X_pad, a.S_pad, a.D_pad,
-                                     a.T_pad, RB, EB, int(sizeof(Real)));
+                                     a.T_pad, RB, EB, int(sizeof(Real)), XDB ? 2 : 1);
   unsigned char *smem = smem_all + lay.total * gid;
   double *dscr = reinterpret_cast<double *>(smem);
   long long *lscr = reinterpret_cast<long long *>(smem + 256);
@@ -139,6 +150,17 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   // Snake order: round r gives warp w tile r*NW + w (r even) or r*NW + NW-1-w
   // (r odd), pairing heavy and light tiles (tiles are sorted by degree).
   auto tile_of = [&](int r) { return r * NW + ((r & 1) ? NW - 1 - warp : warp); };
+  // XDB: this warp's tiles are wl[wlo..whi) (host LPT lists, staged per phase).
+  const int *wl = reinterpret_cast<const int *>(smem + lay.wlist);
+  const int *wt = reinterpret_cast<const int *>(smem + lay.wtab);
+  int wlo = 0, whi = nrounds;
+  auto read_warps = [&] {
+    if constexpr (XDB) {
+      wlo = wt[warp];
+      whi = wt[warp + 1];
+    }
+  };
+  auto tile_at = [&](int i) { return XDB ? wl[i] : tile_of(i); };
 
   // Arc-pack views of the current phase: shared memory (denominator) or L1 (numerators).
   const unsigned *tinfo;
@@ -176,6 +198,12 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       copy16<GROUP>(ti, gi, size_t(ntiles) * 128, tid);
       copy16<GROUP>(tt, gt, size_t(pad4(ntiles)) * 4, tid);
       copy16<GROUP>(tb, gb, size_t(pad4(ntiles)) * 4, tid);
+      if constexpr (XDB) {
+        copy16<GROUP>(smem + lay.wlist, (fwd ? a.g.tf_wlist : a.g.tb_wlist) + toff,
+                      size_t(pad4(ntiles)) * 4, tid);
+        copy16<GROUP>(smem + lay.wtab, (fwd ? a.g.tf_wtab : a.g.tb_wtab) + desc[kWTabOff],
+                      size_t(kWarpTable) * 4, tid);
+      }
       tinfo = ti;
       ttrips = tt;
       tbase = tb;
@@ -269,6 +297,8 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     if (rep2) v[rstride + s] = x;
   };
   // ---- prologue -----------------------------------------------------------------
+  for (int i = tid; i < 2 * RB; i += GROUP) rbuf[i] = Real(0);  // padding lanes stay 0
+  gsync();
   for (int s = tid; s < S; s += GROUP) put_vec(rbuf, s, (s == init) ? Real(1) : Real(0));
   issue_row(0);
   issue_row(1);
@@ -279,6 +309,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   gsync();
   compute_e(0, true);
   gsync();
+  read_warps();
 
   // ---- forward: one barrier per frame ------------------------------------------------
   Real inv2 = Real(1), leakc = Real(0);
@@ -305,6 +336,18 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       Real *arow = trellis + size_t(k) * S_pad;
       if constexpr (CUSTOM_PI) {
         for (int s = tid; s < S; s += GROUP) arow[s] = (r[s] + leakc * pi[s]) * inv2;
+      } else if constexpr (FAST) {  // float4: S_pad and both row bases are 16-byte multiples
+        const float4 *r4 = reinterpret_cast<const float4 *>(r);
+        float4 *a4 = reinterpret_cast<float4 *>(arow);
+        const float lu = leakc * upi;
+        for (int q = tid; q < (S_pad >> 2); q += GROUP) {
+          float4 v = r4[q];
+          v.x = (v.x + lu) * inv2;
+          v.y = (v.y + lu) * inv2;
+          v.z = (v.z + lu) * inv2;
+          v.w = (v.w + lu) * inv2;
+          a4[q] = v;
+        }
       } else {
         const Real lu = leakc * upi;
         for (int s = tid; s < S; s += GROUP) arow[s] = (r[s] + lu) * inv2;
@@ -322,9 +365,9 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       (void)e32;
       (void)r32;
       Real psum = Real(0);
-      for (int rr = 0; rr < nrounds; ++rr) {
-        const int tile = tile_of(rr);
-        if (tile >= ntiles) continue;
+      for (int rr = wlo; rr < whi; ++rr) {
+        const int tile = tile_at(rr);
+        if (!XDB && tile >= ntiles) continue;
         const unsigned info = tinfo[tile * 32 + lane];
         const int trips = ttrips[tile];
         const int base = tbase[tile] + lane;
@@ -425,7 +468,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     const int *pp = a.g.pdf_arc_ptr + desc[kPdfPtrOff2];
     for (int d = tid; d <= D; d += GROUP) pdfptr[d] = pp[d];
     // Padding slots of the per-pdf groups are never written: zero them once.
-    for (int i = tid; i < X_pad; i += GROUP) xterm[i] = Real(0);
+    for (int i = tid; i < (XDB ? 2 : 1) * X_pad; i += GROUP) xterm[i] = Real(0);
   }
   auto issue_alpha = [&](int k) {
     if (k < 0) return;
@@ -445,7 +488,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     spl <<= 1;
     ++spl_log;
   }
-  auto flush_post = [&](int t) {
+  auto flush_post = [&](int t, const Real *xsrc) {
     Real *prow = post_b + size_t(t) * D;
     const Real *old = gstage + (t & 1) * D_pad;
     const int sub = ctid & (spl - 1);
@@ -455,7 +498,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       Real g = Real(0);
       if (d < D) {
         const int lo = pdfptr[d] >> 2, hi = pdfptr[d + 1] >> 2;
-        for (int q = lo + sub; q < hi; q += spl) g += sum_groups4(xterm + 4 * q, 1);
+        for (int q = lo + sub; q < hi; q += spl) g += sum_groups4(xsrc + 4 * q, 1);
       }
       for (int o = 1; o < spl; o <<= 1) g += __shfl_xor_sync(kFull, g, o);
       if (d < D && sub == 0) {
@@ -480,12 +523,17 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   gsync();
   compute_e(T - 1, false);
   gsync();
+  read_warps();
 
+  const bool flusher = cwarp * 32 < D * spl;
   for (int t = T; t >= 1; --t) {
     const int ct = t & 1, cp = ct ^ 1;
     Real ld = Real(0);
     if (t < T && lam > Real(0)) ld = lam * lane_sum<NW>(part + ct * 32, lane);
     const Real inv = rcp_rn(scales[t - 1]);
+    // XDB: slots of frame t-1 go to buffer (t & 1); flush frame t (the other one) now.
+    const int xb = XDB ? ct : 0;
+    if (XDB && t < T && flusher) flush_post(t, xterm + (xb ^ 1) * X_pad);
     if (t - 2 >= 0) compute_e(t - 2, false);
     issue_row(t - 3);
     issue_alpha(t - 2);
@@ -496,11 +544,11 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       const Real *e = ebuf + cp * EB;
       const Real *al = aring + cp * S_pad;  // alpha_{t-1}
       Real *bn = rbuf + cp * RB;
-      Real *xt = xterm;
+      Real *xt = xterm + xb * X_pad;
       Real dp = Real(0);
-      for (int rr = 0; rr < nrounds; ++rr) {
-        const int tile = tile_of(rr);
-        if (tile >= ntiles) continue;
+      for (int rr = wlo; rr < whi; ++rr) {
+        const int tile = tile_at(rr);
+        if (!XDB && tile >= ntiles) continue;
         const unsigned info = tinfo[tile * 32 + lane];
         const int trips = ttrips[tile];
         const int base = tbase[tile] + lane;
@@ -533,18 +581,21 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     cp_async_wait<0>();
     row_max_part(t - 3);
     gsync();
-    // The posterior slots of frame t-1 are complete: write its gradient row,
-    // then release the (single) slot buffer for the next frame.
-    if (cwarp * 32 < D * spl) flush_post(t - 1);
-    gsync();
+    if (!XDB) {
+      // The posterior slots of frame t-1 are complete: write its gradient row,
+      // then release the (single) slot buffer for the next frame.
+      if (flusher) flush_post(t - 1, xterm);
+      gsync();
+    }
   }
+  if (XDB && flusher) flush_post(0, xterm + X_pad);  // frame 0: written at t = 1
 }
 
-template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI>
+template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI, bool XDB = false>
 static int launch_tile_impl2(const FBArgs<Real> &a, const lfmmi_graphs *g, size_t per_item,
                              cudaStream_t st) {
   static bool configured = false;
-  auto kern = fb_tile_kernel<Real, GROUP, IPC, SMEM_GRAPH, CUSTOM_PI>;
+  auto kern = fb_tile_kernel<Real, GROUP, IPC, SMEM_GRAPH, CUSTOM_PI, XDB>;
   if (!configured) {
     int rc = check_cuda(
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
@@ -602,6 +653,16 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
   }
   const size_t per = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
                                  a.T_pad, a.rep_r * a.r_stride, a.rep_e * a.e_stride, real).total;
+  if constexpr (std::is_same<Real, float>::value) {
+    const size_t per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
+                                    a.T_pad, a.rep_r * a.r_stride, a.rep_e * a.e_stride, real, 2)
+                            .total;
+    if (std::getenv("LFMMI_DEBUG"))
+      std::fprintf(stderr, "[lfmmi] den tile smem single=%zu double=%zu limit=%d\n", per, per2,
+                   kMaxSmem);
+    if (!a.leak_pi && per2 <= size_t(kMaxSmem) && !std::getenv("LFMMI_TILE_SINGLE_X"))
+      return launch_tile_impl2<float, kDenGroup, 1, true, false, true>(a, g, per2, st);
+  }
   if (per > size_t(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "tile pack needs " + std::to_string(per) + " B shared memory");

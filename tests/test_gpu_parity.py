@@ -116,11 +116,13 @@ def test_three_phase_api(cuda, name):
 
 
 # ------------------------------------------------- BASELINE configs vs oracle
-@pytest.mark.parametrize("kernel", ["auto", "fused", "fused1x", "group"])
+@pytest.mark.parametrize("kernel", ["auto", "tile1x", "fused", "fused1x", "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])
 def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
+    if kernel == "tile1x":  # denominator tile kernel with a single posterior slot buffer
+        monkeypatch.setenv("LFMMI_TILE_SINGLE_X", "1")
     if kernel in ("fused", "fused1x"):  # single-launch num+den+grad kernel (opt-in)
         monkeypatch.setenv("LFMMI_FUSED", "1")
     if kernel == "fused1x":  # ... with a single posterior slot buffer
