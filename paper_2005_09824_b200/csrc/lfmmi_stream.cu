@@ -43,7 +43,7 @@ namespace lfmmi {
 namespace {
 
 constexpr int kStreamThreads = 1024;
-constexpr int kEPT = 2;  // log-likelihood elements per thread (D <= 2048)
+constexpr int kMaxD = 2048;  // log-likelihood row held in registers: kMaxD / NT per thread
 constexpr float kPostScale = 268435456.f;  // 2^28: posterior bins in uint32 fixed point
 
 struct StreamLayout {
@@ -80,9 +80,10 @@ __device__ __forceinline__ uint2 ldg_slot(const uint2 *p) {
 }  // namespace
 
 template <int NT, int CL>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, 1024 / NT)
     fb_stream_kernel(const FBArgs<float> a, int S32, const StreamLayout lay) {
   constexpr int NW = NT / 32;
+  constexpr int kEPT = kMaxD / NT;  // log-likelihood elements per thread
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x / CL;
@@ -414,10 +415,10 @@ int launch_stream(const FBArgs<Real> &, const lfmmi_graphs *, cudaStream_t) {
   return set_error(LFMMI_ERR_UNSUPPORTED, "stream kernel is fp32-only");
 }
 
-template <int CL>
+template <int NT, int CL>
 static int launch_stream_impl(const FBArgs<float> &a, int S32, const StreamLayout &lay,
                               cudaStream_t st) {
-  auto kern = fb_stream_kernel<kStreamThreads, CL>;
+  auto kern = fb_stream_kernel<NT, CL>;
   static bool configured = false;
   if (!configured) {
     int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -428,7 +429,7 @@ static int launch_stream_impl(const FBArgs<float> &a, int S32, const StreamLayou
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.B * CL);
-  cfg.blockDim = dim3(kStreamThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = lay.total;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -445,8 +446,7 @@ template <>
 int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st) {
   if (!g->streamable) return set_error(LFMMI_ERR_UNSUPPORTED, "graph has no stream pack");
   if (a.leak_pi) return set_error(LFMMI_ERR_UNSUPPORTED, "stream kernel: uniform leak only");
-  if (a.D > kEPT * kStreamThreads)
-    return set_error(LFMMI_ERR_UNSUPPORTED, "stream kernel: D > 2048");
+  if (a.D > kMaxD) return set_error(LFMMI_ERR_UNSUPPORTED, "stream kernel: D > 2048");
   if (a.mode != kPostWrite && a.mode != kPostNegate)
     return set_error(LFMMI_ERR_UNSUPPORTED, "stream kernel: WRITE / NEGATE modes only");
   const int S32 = (g->max_states + 31) & ~31;
@@ -454,14 +454,17 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   if (lay.total > unsigned(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "stream kernel needs " + std::to_string(lay.total) + " B shared memory");
-  // Two SMs per utterance (2-CTA cluster) while the batch leaves SMs idle.
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const char *env = std::getenv("LFMMI_STREAM_CLUSTER");
-  const int cl = env ? std::atoi(env) : (2 * a.B <= sms ? 2 : 1);
-  if (cl == 2) return launch_stream_impl<2>(a, S32, lay, st);
-  return launch_stream_impl<1>(a, S32, lay, st);
+  // Two SMs per utterance (2-CTA cluster of 1024-thread CTAs) while the batch
+  // leaves SMs idle, else one 1024-thread CTA per utterance.  ("512x2" — two
+  // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
+  const char *env = std::getenv("LFMMI_STREAM_MODE");  // "1024x1", "1024x2", "512x2"
+  std::string mode = env ? env : (2 * a.B <= sms ? "1024x2" : "1024x1");
+  if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, S32, lay, st);
+  if (mode == "512x2") return launch_stream_impl<512, 2>(a, S32, lay, st);
+  return launch_stream_impl<1024, 1>(a, S32, lay, st);
 }
 
 template int launch_stream<double>(const FBArgs<double> &, const lfmmi_graphs *, cudaStream_t);

@@ -139,7 +139,7 @@ def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
     assert res.num_failed == ref.num_failed == 0
 
 
-@pytest.mark.parametrize("kernel", ["stream", "stream1", "group"])
+@pytest.mark.parametrize("kernel", ["stream", "stream1", "stream512", "group"])
 def test_large_graph_l2_path_vs_oracle(cuda, kernel, monkeypatch):
     """Config 4 (20k states / 200k arcs / 2000 pdfs): the arc packs do not fit in
     shared memory.  "stream": coalesced 32-state tiles streamed from L2
@@ -148,7 +148,9 @@ def test_large_graph_l2_path_vs_oracle(cuda, kernel, monkeypatch):
     if kernel == "group":
         monkeypatch.setenv("LFMMI_DISABLE_STREAM", "1")
     if kernel == "stream1":  # one CTA per utterance instead of a 2-CTA cluster
-        monkeypatch.setenv("LFMMI_STREAM_CLUSTER", "1")
+        monkeypatch.setenv("LFMMI_STREAM_MODE", "1024x1")
+    if kernel == "stream512":  # 2-CTA clusters of 512 threads (two per SM when they fit)
+        monkeypatch.setenv("LFMMI_STREAM_MODE", "512x2")
     w = synth.make_workload("large", seed=3, batch_size=2)
     batch, nums, den = w.build(P)
     res = P.chain_loss(batch, nums, den)
