@@ -221,7 +221,8 @@ template <typename Real>
 int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_max, int D,
               const void *L, const int *lengths, double leak, double floor, const void *leak_pi,
               void *work, size_t work_bytes, void *post, int mode, const int *other_fail,
-              double *logp, int *fail, double *scale_logs, cudaStream_t st, bool packed) {
+              double *logp, int *fail, double *scale_logs, cudaStream_t st, bool packed,
+              int64_t total_frames) {
   FBArgs<Real> a{};
   a.g = graphs->dev;
   a.row_map = row_map;
@@ -248,6 +249,12 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
   a.scale_logs = scale_logs;
   a.I_pad = pad4(std::max(1, graphs->max_arcs));
   a.packed = packed ? 1 : 0;
+  {
+    const long long tf = std::max<long long>(total_frames, 1);
+    const long long stride = (std::max(1, int(graphs->max_states)) + 31) & ~31;
+    a.sc_off = stride * tf;  // after the (round32-strided) trellis region
+    a.sc_total = tf;
+  }
   if (std::is_same<Real, float>::value) {  // f32 tile slots address replicated vectors
     a.rep_r = graphs->rep_r;
     a.r_stride = graphs->r_stride;
@@ -285,9 +292,10 @@ using namespace lfmmi;
 extern "C" size_t lfmmi_workspace_size(int32_t max_states, int64_t total_frames,
                                        int32_t precision) {
   const size_t es = precision == LFMMI_F64 ? 8 : 4;
-  // Row stride round32(S): the stream kernel spills alpha in 32-state tile order.
+  // Row stride round32(S): the stream kernel spills alpha in 32-state tile order;
+  // + 2 Reals per frame for the per-frame scales and row maxima (tile kernel).
   const size_t stride = size_t((std::max(1, int(max_states)) + 31) & ~31);
-  return stride * size_t(std::max<int64_t>(total_frames, 1)) * es + 256;
+  return (stride + 2) * size_t(std::max<int64_t>(total_frames, 1)) * es + 256;
 }
 
 static int check_common(const lfmmi_graphs *graphs, int32_t batch, int32_t max_frames,
@@ -329,10 +337,11 @@ static int forward_backward_impl(const lfmmi_graphs *graphs, const int64_t *row_
     return run_fused<double>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
                              scale_floor, leak_pi, workspace, workspace_bytes, posteriors,
                              post_mode, other_fail, log_probs, fail_frames, scale_logs, st,
-                             packed);
+                             packed, total_frames);
   return run_fused<float>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
                           scale_floor, leak_pi, workspace, workspace_bytes, posteriors, post_mode,
-                          other_fail, log_probs, fail_frames, scale_logs, st, packed);
+                          other_fail, log_probs, fail_frames, scale_logs, st, packed,
+                          total_frames);
 }
 
 

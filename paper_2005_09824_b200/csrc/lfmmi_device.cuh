@@ -89,6 +89,8 @@ struct FBArgs {
   int I_pad;  // tile kernel: per-arc scratch (posterior slots)
   int rep_r, r_stride, rep_e, e_stride;  // tile kernel: gather-vector replication
   int packed;  // 1: L / posteriors are ragged (sum_b T_b, D), item b at row sum_{j<b} T_j
+  long long sc_off;    // tile kernel: per-frame scales at work + sc_off + item_off,
+  long long sc_total;  //   row maxima sc_total Reals further (ragged, like the trellis)
 };
 
 }  // namespace lfmmi

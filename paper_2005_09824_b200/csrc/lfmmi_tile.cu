@@ -67,8 +67,8 @@ __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int
   l.ebuf = o;    o = al16(o + size_t(2) * EB * real);     // emission rows x copies
   l.stage = o;   o = al16(o + size_t(4) * D_pad * real);
   l.gstage = o;  o = al16(o + size_t(2) * D_pad * real);
-  l.scales = o;  o = al16(o + size_t(T_pad) * real);
-  l.shifts = o;  o = al16(o + size_t(T_pad) * real);
+  l.scales = o;  // per-frame scales / row maxima live in the HBM workspace (ragged)
+  l.shifts = o;
   l.part = o;    o = al16(o + size_t(2) * 32 * real);
   l.mpart = o;   o = al16(o + size_t(2) * 32 * real);
   l.total = o;
@@ -120,8 +120,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   Real *ebuf = reinterpret_cast<Real *>(smem + lay.ebuf);
   Real *stage = reinterpret_cast<Real *>(smem + lay.stage);
   Real *gstage = reinterpret_cast<Real *>(smem + lay.gstage);
-  Real *scales = reinterpret_cast<Real *>(smem + lay.scales);
-  Real *shifts = reinterpret_cast<Real *>(smem + lay.shifts);
+  Real *scales = nullptr, *shifts = nullptr;  // set once item_off is known
   Real *part = reinterpret_cast<Real *>(smem + lay.part);
   Real *mpart = reinterpret_cast<Real *>(smem + lay.mpart);
   auto gsync = [] { tsync<GROUP, IPC>(); };
@@ -245,6 +244,8 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   const Real pisum = pi ? Real(pisum_d) : Real(1);
   const Real lam = a.leak;
   Real *trellis = a.work + item_off * S_pad;
+  scales = a.work + a.sc_off + item_off;
+  shifts = scales + a.sc_total;
   if (a.packed) {  // ragged layout: item b's rows start at sum_{j<b} T_j
     Lb = a.L + size_t(item_off) * D;
     post_b = a.post + size_t(item_off) * D;
@@ -526,11 +527,14 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   read_warps();
 
   const bool flusher = cwarp * 32 < D * spl;
+  Real sc_cur = scales[T - 1];
   for (int t = T; t >= 1; --t) {
     const int ct = t & 1, cp = ct ^ 1;
     Real ld = Real(0);
     if (t < T && lam > Real(0)) ld = lam * lane_sum<NW>(part + ct * 32, lane);
-    const Real inv = rcp_rn(scales[t - 1]);
+    // scales[t-1] was read one iteration ahead (global, off the critical path)
+    const Real inv = rcp_rn(sc_cur);
+    sc_cur = t >= 2 ? scales[t - 2] : Real(1);
     // XDB: slots of frame t-1 go to buffer (t & 1); flush frame t (the other one) now.
     const int xb = XDB ? ct : 0;
     if (XDB && t < T && flusher) flush_post(t, xterm + (xb ^ 1) * X_pad);
@@ -638,7 +642,9 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     // Utterances fewer than SMs: more threads per numerator shorten its
     // per-frame latency chain (it runs next to the denominator pass).
     const char *ng = std::getenv("LFMMI_NUM_GROUP");
-    const int want = ng ? std::atoi(ng) : (a.B < 2 * 148 ? 128 : 32);
+    // 4 warps per numerator at every batch size: sweep (B = 1024) num pass
+    // 7.8 ms vs 16.0 ms with one warp per utterance.
+    const int want = ng ? std::atoi(ng) : 128;
     if (want == 128 && per_s <= size_t(kMaxSmem))
       return launch_tile_impl<Real, 128, 1, true>(a, g, per_s, st);
     if (want == 64 && per_s <= size_t(kMaxSmem))
