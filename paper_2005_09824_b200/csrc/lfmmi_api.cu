@@ -254,6 +254,7 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
     const long long stride = (std::max(1, int(graphs->max_states)) + 31) & ~31;
     a.sc_off = stride * tf;  // after the (round32-strided) trellis region
     a.sc_total = tf;
+    a.sc_smem = 1;  // default: shared memory (the den XDB launcher may move them to HBM)
   }
   if (std::is_same<Real, float>::value) {  // f32 tile slots address replicated vectors
     a.rep_r = graphs->rep_r;

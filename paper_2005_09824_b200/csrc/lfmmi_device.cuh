@@ -91,6 +91,7 @@ struct FBArgs {
   int packed;  // 1: L / posteriors are ragged (sum_b T_b, D), item b at row sum_{j<b} T_j
   long long sc_off;    // tile kernel: per-frame scales at work + sc_off + item_off,
   long long sc_total;  //   row maxima sc_total Reals further (ragged, like the trellis)
+  int sc_smem;         //   ... or in shared memory (1; set by the launcher when they fit)
 };
 
 }  // namespace lfmmi

@@ -48,7 +48,8 @@ struct TileLayout {  // byte offsets of one utterance's slice of shared memory
 
 __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int ntiles, int D,
                                                   int X_pad, int S_pad, int D_pad, int T_pad,
-                                                  int RB, int EB, int real, int nx = 1) {
+                                                  int RB, int EB, int real, int nx = 1,
+                                                  bool smem_scales = true) {
   TileLayout l;
   size_t o = 512;  // scratch: 32 doubles + 32 int64
   const size_t F = smem_graph ? size_t(Fmax) : 0;
@@ -67,8 +68,10 @@ __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int
   l.ebuf = o;    o = al16(o + size_t(2) * EB * real);     // emission rows x copies
   l.stage = o;   o = al16(o + size_t(4) * D_pad * real);
   l.gstage = o;  o = al16(o + size_t(2) * D_pad * real);
-  l.scales = o;  // per-frame scales / row maxima live in the HBM workspace (ragged)
-  l.shifts = o;
+  // per-frame scales / row maxima: shared memory when they fit (smem_scales),
+  // else the HBM workspace (ragged, like the trellis)
+  l.scales = o;  o = al16(o + (smem_scales ? size_t(T_pad) * real : 0));
+  l.shifts = o;  o = al16(o + (smem_scales ? size_t(T_pad) * real : 0));
   l.part = o;    o = al16(o + size_t(2) * 32 * real);
   l.mpart = o;   o = al16(o + size_t(2) * 32 * real);
   l.total = o;
@@ -109,7 +112,8 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   if (b >= a.B) return;  // whole group exits together (no CTA-wide barriers for IPC > 1)
   const int RB = a.rep_r * a.r_stride, EB = a.rep_e * a.e_stride;
   const TileLayout lay = tile_layout(SMEM_GRAPH, Fmax, ntiles_max, a.D, X_pad, a.S_pad, a.D_pad,
-                                     a.T_pad, RB, EB, int(sizeof(Real)), XDB ? 2 : 1);
+                                     a.T_pad, RB, EB, int(sizeof(Real)), XDB ? 2 : 1,
+                                     a.sc_smem != 0);
   unsigned char *smem = smem_all + lay.total * gid;
   double *dscr = reinterpret_cast<double *>(smem);
   long long *lscr = reinterpret_cast<long long *>(smem + 256);
@@ -244,8 +248,13 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   const Real pisum = pi ? Real(pisum_d) : Real(1);
   const Real lam = a.leak;
   Real *trellis = a.work + item_off * S_pad;
-  scales = a.work + a.sc_off + item_off;
-  shifts = scales + a.sc_total;
+  if (a.sc_smem) {
+    scales = reinterpret_cast<Real *>(smem + lay.scales);
+    shifts = reinterpret_cast<Real *>(smem + lay.shifts);
+  } else {
+    scales = a.work + a.sc_off + item_off;
+    shifts = scales + a.sc_total;
+  }
   if (a.packed) {  // ragged layout: item b's rows start at sum_{j<b} T_j
     Lb = a.L + size_t(item_off) * D;
     post_b = a.post + size_t(item_off) * D;
@@ -660,14 +669,24 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
   const size_t per = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
                                  a.T_pad, a.rep_r * a.r_stride, a.rep_e * a.e_stride, real).total;
   if constexpr (std::is_same<Real, float>::value) {
-    const size_t per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
-                                    a.T_pad, a.rep_r * a.r_stride, a.rep_e * a.e_stride, real, 2)
-                            .total;
+    // Double-buffered slots first; per-frame scales in shared memory if they
+    // still fit (short utterances), else in the HBM workspace.
+    FBArgs<float> b = a;
+    b.sc_smem = 1;
+    size_t per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad, a.T_pad,
+                              a.rep_r * a.r_stride, a.rep_e * a.e_stride, real, 2, true)
+                      .total;
+    if (per2 > size_t(kMaxSmem) || std::getenv("LFMMI_GLOBAL_SCALES")) {
+      b.sc_smem = 0;
+      per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad, a.T_pad,
+                         a.rep_r * a.r_stride, a.rep_e * a.e_stride, real, 2, false)
+                 .total;
+    }
     if (std::getenv("LFMMI_DEBUG"))
       std::fprintf(stderr, "[lfmmi] den tile smem single=%zu double=%zu limit=%d\n", per, per2,
                    kMaxSmem);
     if (!a.leak_pi && per2 <= size_t(kMaxSmem) && !std::getenv("LFMMI_TILE_SINGLE_X"))
-      return launch_tile_impl2<float, kDenGroup, 1, true, false, true>(a, g, per2, st);
+      return launch_tile_impl2<float, kDenGroup, 1, true, false, true>(b, g, per2, st);
   }
   if (per > size_t(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,
