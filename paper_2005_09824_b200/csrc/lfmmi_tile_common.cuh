@@ -105,6 +105,7 @@ template <bool LEAKY>
 __device__ __forceinline__ void fwd_tile_f32(uint32_t sb, int trips, uint32_t e32, uint32_t r32,
                                              float &A, float &Bs) {
   int j = 0;
+#pragma unroll 1
   for (; j + 4 <= trips; j += 4, sb += 4 * 256) {
     const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
                 w3 = lds_v2(sb + 768);
@@ -146,6 +147,7 @@ __device__ __forceinline__ float bwd_tile_f32(uint32_t sb, uint32_t xb, int trip
                                               uint32_t b32, uint32_t x32, float ld, float as) {
   float A = 0.f;
   int j = 0;
+#pragma unroll 1
   for (; j + 4 <= trips; j += 4, sb += 4 * 256, xb += 4 * 64) {
     const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
                 w3 = lds_v2(sb + 768);
