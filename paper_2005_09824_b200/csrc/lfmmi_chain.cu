@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(GROUP, 1)
     if (t < 0 || t >= T || cwarp >= nrw || skip(6)) return;
     const float *src = stage + (t & (kStageRing - 1)) * D_pad;
     float mx = -INFINITY;
-    for (int d = ctid; d < D; d += GROUP) mx = fmaxf(mx, src[d]);
+    for (int d = ctid; d < D; d += GROUP) mx = nan_max(mx, src[d]);
     mx = warp_max(mx);
     if (lane == 0) mpart[(t & 1) * 32 + cwarp] = mx;
   };

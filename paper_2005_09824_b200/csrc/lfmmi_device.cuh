@@ -20,10 +20,23 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// NaN-propagating maximum: the reference takes row maxima with numpy
+// (forward_backward.py:126), where a NaN anywhere in a valid frame makes the
+// shift NaN, every emission of the frame NaN and the utterance fail in both
+// graphs.  IEEE fmax would drop the NaN and only poison that one pdf.
+__device__ __forceinline__ float nan_max(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ double nan_max(double a, double b) {
+  return (a != a || b != b) ? (a + b) : fmax(a, b);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_max(T v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = nan_max(v, __shfl_xor_sync(kFull, v, o));
   return v;
 }
 

@@ -163,13 +163,13 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
     if (t < 0 || t >= T) return;
     const Real *src = stage + (t & 3) * D_pad;
     Real m = -INFINITY;
-    for (int d = tid; d < D; d += GROUP) m = fmax(m, src[d]);
+    for (int d = tid; d < D; d += GROUP) m = nan_max(m, src[d]);
     m = warp_max(m);
     if (lane == 0) mpart[(t & 1) * NW + warp] = m;
   };
   auto block_max = [&](int t) {
     Real m = -INFINITY;
-    for (int w = 0; w < NW; ++w) m = fmax(m, mpart[(t & 1) * NW + w]);
+    for (int w = 0; w < NW; ++w) m = nan_max(m, mpart[(t & 1) * NW + w]);
     return m;
   };
   auto compute_e = [&](int t, bool record_shift) {  // e_t -> ebuf[t & 1]
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
     // valid frame); remaining scales stay 1 (forward_backward.py:184,206).
     for (int k = fail_at + 1 + warp; k < T; k += NW) {
       Real m = -INFINITY;
-      for (int d = lane; d < D; d += 32) m = fmax(m, Lb[size_t(k) * D + d]);
+      for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
       m = warp_max(m);
       if (lane == 0) shifts[k] = m;
     }

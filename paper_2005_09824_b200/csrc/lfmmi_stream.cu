@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   auto max_part = [&](int t, const float *r) {  // warp maxima of row t -> mpart[t & 1]
     float m = r[0];
 #pragma unroll
-    for (int j = 1; j < kEPT; ++j) m = fmaxf(m, r[j]);
+    for (int j = 1; j < kEPT; ++j) m = nan_max(m, r[j]);
     m = warp_max(m);
     if (lane == 0) mpart[(t & 1) * 32 + warp] = m;
   };
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   if (fail_at >= 0) {
     for (int k = fail_at + 1 + warp; k < T; k += NW) {
       float m = -INFINITY;
-      for (int d = lane; d < D; d += 32) m = fmaxf(m, Lb[size_t(k) * D + d]);
+      for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
       m = warp_max(m);
       if (lane == 0) shifts[k] = m;
     }

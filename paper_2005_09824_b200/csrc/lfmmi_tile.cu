@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     if (t < 0 || t >= T || cwarp >= nrw) return;
     const Real *src = stage + (t & 3) * D_pad;
     Real m = -INFINITY;
-    for (int d = ctid; d < D; d += GROUP) m = fmax(m, src[d]);
+    for (int d = ctid; d < D; d += GROUP) m = nan_max(m, src[d]);
     m = warp_max(m);
     if (lane == 0) mpart[(t & 1) * 32 + cwarp] = m;
   };
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     // maxima, remaining scales stay 1 (forward_backward.py:184,206).
     for (int k = fail_at + 1 + warp; k < T; k += NW) {
       Real m = -INFINITY;
-      for (int d = lane; d < D; d += 32) m = fmax(m, Lb[size_t(k) * D + d]);
+      for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
       m = warp_max(m);
       if (lane == 0) shifts[k] = m;
     }

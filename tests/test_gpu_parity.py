@@ -236,6 +236,37 @@ def test_failure_semantics(cuda):
     assert math.isnan(num_lp) and not math.isnan(den_lp)
 
 
+@pytest.mark.parametrize("config,batch_size,kernel", [
+    ("wsj_mono", 4, "auto"), ("wsj_mono", 4, "tile1x"), ("wsj_mono", 4, "fused"),
+    ("wsj_biphone", 3, "auto"), ("large", 2, "auto"), ("large", 2, "stream1")])
+def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kernel, monkeypatch):
+    """A NaN log-likelihood makes that utterance's column totals NaN -> it fails
+    at that frame in both graphs (_kernels.py:114-118); the others are untouched
+    and chain_loss excludes it (loss.py:61-69).  Covers the early-exit paths of
+    the XDB tile kernel, the fused kernel and the 1- and 2-CTA stream kernel."""
+    if kernel == "tile1x":
+        monkeypatch.setenv("LFMMI_TILE_SINGLE_X", "1")
+    if kernel == "fused":
+        monkeypatch.setenv("LFMMI_FUSED", "1")
+    if kernel == "stream1":
+        monkeypatch.setenv("LFMMI_STREAM_MODE", "1024x1")
+    w = synth.make_workload(config, seed=9, batch_size=batch_size)
+    batch, nums, den = w.build(P)  # make_batch rejects non-finite input: poison afterwards
+    bad = 1
+    values = np.array(batch.values)
+    values[bad, 5, 3] = np.nan
+    batch = P.LogLikBatch(values=values, lengths=batch.lengths,
+                          valid_batch_sizes=batch.valid_batch_sizes, order_map=batch.order_map)
+    res = P.chain_loss(batch, nums, den)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    assert res.num_failed == ref.num_failed == 1
+    assert np.all(res.grad[bad] == 0.0)
+    n, d = res.per_utt[bad]
+    assert math.isnan(n) and math.isnan(d)
+    assert _rel(res.objective, ref.objective) <= FP32_OBJ_REL
+    assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
+
+
 def test_custom_leak_distribution(cuda):
     w = synth.make_workload("toy", seed=5)
     batch, nums, den = w.build(P)
