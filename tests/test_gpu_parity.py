@@ -267,6 +267,22 @@ def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kern
     assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
 
 
+@pytest.mark.parametrize("mode", ["1024x1", "1024x2"])
+def test_stream_kernel_short_utterances(cuda, mode, monkeypatch):
+    """1-, 2- and 3-frame utterances through the L2-streamed kernel (biphone-sized
+    denominator): prologue / epilogue edges of the register row pipeline."""
+    monkeypatch.setenv("LFMMI_STREAM_MODE", mode)
+    w = synth.make_workload("wsj_biphone", seed=10, batch_size=4)
+    rng = np.random.default_rng(0)
+    seqs = [rng.normal(0, 2, (t, w.D)).astype(np.float32).astype(np.float64) for t in (1, 2, 3, 7)]
+    batch = P.make_batch(seqs)
+    den = P.ChainGraphBatch.broadcast(w.den_graph(P), 4)
+    fb = P.forward_backward(batch, den)
+    rf = O.forward_backward(batch, den, leak=1e-5)
+    np.testing.assert_allclose(fb.log_probs, rf.log_probs, rtol=1e-6, atol=1e-6)
+    assert np.abs(fb.posteriors - rf.posteriors).max() <= FP32_GRAD_ABS
+
+
 def test_custom_leak_distribution(cuda):
     w = synth.make_workload("toy", seed=5)
     batch, nums, den = w.build(P)
