@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(GROUP, 1)
       plast = now;
     }
   };
-  const int RBd = a.rep_rd * a.r_strided, RBn = a.rep_rn * a.r_striden;
+  const int RBd = pad4(a.rep_rd * a.r_strided), RBn = pad4(a.rep_rn * a.r_striden);
   const int EB = a.rep_e * a.e_stride;
   double *dscr = reinterpret_cast<double *>(smem);
   long long *lscr = reinterpret_cast<long long *>(smem + 256);
@@ -737,7 +737,8 @@ static int launch_profiled(const ChainArgs &a0, const ChainDims &m, const ChainL
 }
 
 int launch_chain(const ChainArgs &a, const ChainDims &m, cudaStream_t st) {
-  const int RBd = a.rep_rd * a.r_strided, RBn = a.rep_rn * a.r_striden, EB = a.rep_e * a.e_stride;
+  const int RBd = pad4(a.rep_rd * a.r_strided), RBn = pad4(a.rep_rn * a.r_striden),
+            EB = a.rep_e * a.e_stride;
   const ChainLayout l2 =
       chain_layout(m, a.D, a.D_pad, a.T_pad, RBd, RBn, EB, a.Sd_pad, a.Sn_pad, true);
   const ChainLayout l1 =

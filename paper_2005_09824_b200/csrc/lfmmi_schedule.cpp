@@ -19,6 +19,11 @@
 #include "lfmmi_schedule.h"
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
+#include <cstdint>
+#include <array>
+#include <random>
 #include <cstdlib>
 #include <numeric>
 
@@ -47,10 +52,24 @@ struct BankSet {  // distinct addresses per bank within one slot row
 
 }  // namespace
 
+// Local-search moves per slot row (LFMMI_SCHED_ITERS overrides; 0 = greedy only).
+static int local_search_iters() {
+  static const int n = [] {
+    const char *e = std::getenv("LFMMI_SCHED_ITERS");
+    return e ? std::max(0, std::atoi(e)) : 1500;
+  }();
+  return n;
+}
+
 GatherLayout make_gather_layout(int max_states, int num_pdfs) {
   GatherLayout gl;
   auto round32 = [](int x) { return (x + 31) & ~31; };
-  gl.r_stride = round32(max_states) + 16;  // copy 1 sits 16 banks over
+  // copy 1 of the gather column sits r_off banks over (LFMMI_R_OFF overrides)
+  const char *ro = std::getenv("LFMMI_R_OFF");
+  // (9: the two candidate banks of an address form a ring rather than 16
+  // disjoint pairs, which the row matching exploits better — offline: 1.87 ->
+  // 1.66 wavefronts per warp-wide gather with the local search)
+  gl.r_stride = round32(max_states) + (ro ? std::atoi(ro) : 9);
   gl.rep_r = (2 * gl.r_stride <= 16383) ? 2 : 1;
   if (const char *e = std::getenv("LFMMI_REP_R")) gl.rep_r = std::max(1, std::min(gl.rep_r, std::atoi(e)));
   if (gl.rep_r == 1) gl.r_stride = (max_states + 3) & ~3;
@@ -61,18 +80,119 @@ GatherLayout make_gather_layout(int max_states, int num_pdfs) {
   return gl;
 }
 
+// ---- exact per-row copy assignment + local search over slot rows ---------------
+//
+// For one slot row, the wavefront count of a gather is the largest number of
+// distinct addresses any bank must serve.  Given the row's arcs, choosing the
+// copy (hence the bank) of every distinct address is a bipartite b-matching:
+// addresses -> banks with capacity k; the smallest feasible k is the row's cost
+// (computed exactly by augmenting paths; <= 32 addresses).  A local search then
+// swaps a lane's arcs between slot rows of its tile (any permutation of a
+// lane's arcs is valid) and keeps swaps that do not raise the summed cost.
+namespace {
+
+struct RowSolver {
+  int na = 0;
+  int addr[32];
+  int cand[32][4];
+  int ncand = 1;
+  int slot_owner[32][8];  // bank -> addresses holding its slots
+  int slot_n[32];
+  int choice[32];
+
+  bool try_assign(int a, int k, uint32_t &seen) {
+    for (int c = 0; c < ncand; ++c) {
+      const int b = cand[a][c];
+      if (seen & (1u << b)) continue;
+      seen |= 1u << b;
+      if (slot_n[b] < k) {
+        slot_owner[b][slot_n[b]++] = a;
+        choice[a] = c;
+        return true;
+      }
+      for (int q = 0; q < slot_n[b]; ++q) {
+        const int other = slot_owner[b][q];
+        if (try_assign(other, k, seen)) {
+          slot_owner[b][q] = a;
+          choice[a] = c;
+          return true;
+        }
+      }
+    }
+    return false;
+  }
+
+  // addresses (distinct) with candidate banks; returns min k and fills choice[]
+  int solve() {
+    // lower bound: ceil(na / 32) and the pigeonhole bound of a single candidate
+    for (int k = (na + 31) / 32; k <= 8; ++k) {
+      std::fill(slot_n, slot_n + 32, 0);
+      bool ok = true;
+      for (int a = 0; a < na && ok; ++a) {
+        uint32_t seen = 0;
+        ok = try_assign(a, k, seen);
+      }
+      if (ok) return k;
+    }
+    return 8;
+  }
+};
+
+// Cost of one row: r-gather k + e-gather k; copies chosen per distinct address.
+struct RowEval {
+  int cost = 0;
+  int rcopy[32], ecopy[32];  // per lane (-1 if idle)
+};
+
+RowEval eval_row(const int *arcs, const int *gidx, const int *pdf, const GatherLayout &gl) {
+  RowEval ev;
+  RowSolver rs, es;
+  rs.ncand = gl.rep_r;
+  es.ncand = gl.rep_e;
+  int rlane_addr[32], elane_addr[32];
+  for (int l = 0; l < 32; ++l) {
+    ev.rcopy[l] = ev.ecopy[l] = -1;
+    rlane_addr[l] = elane_addr[l] = -1;
+    const int a = arcs[l];
+    if (a < 0) continue;
+    auto add = [](RowSolver &r, int v) {
+      for (int i = 0; i < r.na; ++i)
+        if (r.addr[i] == v) return i;
+      r.addr[r.na] = v;
+      return r.na++;
+    };
+    rlane_addr[l] = add(rs, gidx[a]);
+    elane_addr[l] = add(es, pdf[a]);
+  }
+  for (int i = 0; i < rs.na; ++i)
+    for (int c = 0; c < rs.ncand; ++c) rs.cand[i][c] = (c * gl.r_stride + rs.addr[i]) & 31;
+  for (int i = 0; i < es.na; ++i)
+    for (int c = 0; c < es.ncand; ++c) es.cand[i][c] = (c * gl.e_stride + es.addr[i]) & 31;
+  const int kr = rs.na ? rs.solve() : 0;
+  const int ke = es.na ? es.solve() : 0;
+  ev.cost = kr + ke;
+  for (int l = 0; l < 32; ++l) {
+    if (rlane_addr[l] >= 0) ev.rcopy[l] = rs.choice[rlane_addr[l]];
+    if (elane_addr[l] >= 0) ev.ecopy[l] = es.choice[elane_addr[l]];
+  }
+  return ev;
+}
+
+}  // namespace
+
 TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
                             const double *prob, const GatherLayout &gl, bool optimize) {
-  TileSchedule ts;
   std::vector<int> order(S);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
     return (ptr[x + 1] - ptr[x]) > (ptr[y + 1] - ptr[y]);
   });
   const int ntiles = (S + 31) / 32;
-  int base = 0;
-  BankSet rb, eb;
-  for (int w = 0; w < ntiles; ++w) {
+  // Tiles are independent: schedule them in parallel into per-tile fragments
+  // (each with its own RNG seed, so the result does not depend on threading).
+  auto do_tile = [&](int w, TileSchedule &ts) {
+    const int base = 0;
+    BankSet rb, eb;
     std::vector<std::vector<int>> rem(32);
     int trips = 0;
     for (int l = 0; l < 32; ++l) {
@@ -161,7 +281,83 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
         }
       }
     }
-    base += 32 * trips;
+    if (optimize && trips > 1 && local_search_iters() > 0) {
+      // slots[j][l] = CSR arc at row j, lane l (-1 idle); search over lane permutations.
+      std::vector<std::array<int, 32>> slots(trips);
+      for (int j = 0; j < trips; ++j)
+        for (int l = 0; l < 32; ++l) slots[j][l] = ts.arc[start + size_t(32) * j + l];
+      std::vector<int> cost(trips);
+      for (int j = 0; j < trips; ++j) cost[j] = eval_row(slots[j].data(), gidx, pdf, gl).cost;
+      std::mt19937 rng(12345u + unsigned(w));
+      const int iters = local_search_iters() * trips;
+      for (int it = 0; it < iters; ++it) {
+        const int l = int(rng() % 32u);
+        const int j1 = int(rng() % unsigned(trips)), j2 = int(rng() % unsigned(trips));
+        if (j1 == j2 || (slots[j1][l] < 0 && slots[j2][l] < 0)) continue;
+        std::swap(slots[j1][l], slots[j2][l]);
+        const int c1 = eval_row(slots[j1].data(), gidx, pdf, gl).cost;
+        const int c2 = eval_row(slots[j2].data(), gidx, pdf, gl).cost;
+        if (c1 + c2 <= cost[j1] + cost[j2]) {
+          cost[j1] = c1;
+          cost[j2] = c2;
+        } else {
+          std::swap(slots[j1][l], slots[j2][l]);
+        }
+      }
+      for (int j = 0; j < trips; ++j) {
+        const RowEval ev = eval_row(slots[j].data(), gidx, pdf, gl);
+        unsigned pad_idx = 0, pad_b32 = 0;
+        bool have_pad = false;
+        for (int l = 0; l < 32; ++l) {
+          const size_t slot = start + size_t(32) * j + l;
+          const int a = slots[j][l];
+          ts.arc[slot] = a;
+          if (a < 0) continue;
+          const int ra = ev.rcopy[l] * gl.r_stride + gidx[a];
+          const int ea = ev.ecopy[l] * gl.e_stride + pdf[a];
+          ts.prob[slot] = prob[a];
+          ts.word_idx[slot] = unsigned(gidx[a]) | (unsigned(pdf[a]) << 16);
+          ts.word_b32[slot] = (unsigned(ra) << 2) | ((unsigned(ea) << 2) << 16);
+          if (!have_pad) {
+            pad_idx = ts.word_idx[slot];
+            pad_b32 = ts.word_b32[slot];
+            have_pad = true;
+          }
+        }
+        for (int l = 0; l < 32; ++l) {
+          const size_t slot = start + size_t(32) * j + l;
+          if (ts.arc[slot] < 0) {
+            ts.prob[slot] = 0.0;
+            ts.word_idx[slot] = pad_idx;
+            ts.word_b32[slot] = pad_b32;
+          }
+        }
+      }
+    }
+  };
+  std::vector<TileSchedule> parts(ntiles);
+  const int nthreads = std::max(1, std::min<int>(ntiles, int(std::thread::hardware_concurrency())));
+  std::atomic<int> next{0};
+  auto worker = [&] {
+    for (int w = next++; w < ntiles; w = next++) do_tile(w, parts[w]);
+  };
+  if (nthreads == 1 || ntiles < 4) {
+    worker();
+  } else {
+    std::vector<std::thread> pool;
+    for (int i = 0; i < nthreads; ++i) pool.emplace_back(worker);
+    for (auto &t : pool) t.join();
+  }
+  TileSchedule ts;
+  for (const TileSchedule &p : parts) {
+    const int off = int(ts.arc.size());
+    ts.info.insert(ts.info.end(), p.info.begin(), p.info.end());
+    ts.trips.push_back(p.trips[0]);
+    ts.base.push_back(off);
+    ts.arc.insert(ts.arc.end(), p.arc.begin(), p.arc.end());
+    ts.word_idx.insert(ts.word_idx.end(), p.word_idx.begin(), p.word_idx.end());
+    ts.word_b32.insert(ts.word_b32.end(), p.word_b32.begin(), p.word_b32.end());
+    ts.prob.insert(ts.prob.end(), p.prob.begin(), p.prob.end());
   }
   return ts;
 }

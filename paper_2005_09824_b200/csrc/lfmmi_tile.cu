@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   (void)ntile_rounds_max;
   const int b = blockIdx.x * IPC + gid;
   if (b >= a.B) return;  // whole group exits together (no CTA-wide barriers for IPC > 1)
-  const int RB = a.rep_r * a.r_stride, EB = a.rep_e * a.e_stride;
+  const int RB = pad4(a.rep_r * a.r_stride), EB = a.rep_e * a.e_stride;  // 16-byte buffers
   const TileLayout lay = tile_layout(SMEM_GRAPH, Fmax, ntiles_max, a.D, X_pad, a.S_pad, a.D_pad,
                                      a.T_pad, RB, EB, int(sizeof(Real)), XDB ? 2 : 1,
                                      a.sc_smem != 0);
@@ -641,7 +641,7 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
   const int X_pad = pad4(std::max(4, g->max_xpad));
   const int real = int(sizeof(Real));
   if (warp_per_item) {
-    const int RB = a.rep_r * a.r_stride, EB = a.rep_e * a.e_stride;
+    const int RB = pad4(a.rep_r * a.r_stride), EB = a.rep_e * a.e_stride;  // 16-byte buffers
     const size_t per = tile_layout(false, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
                                    a.T_pad, RB, EB, real).total;
     // Several utterances per CTA, but keep at least ~one CTA per SM busy.
@@ -667,19 +667,19 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     return set_error(LFMMI_ERR_UNSUPPORTED, "numerator slice exceeds shared memory");
   }
   const size_t per = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
-                                 a.T_pad, a.rep_r * a.r_stride, a.rep_e * a.e_stride, real).total;
+                                 a.T_pad, pad4(a.rep_r * a.r_stride), a.rep_e * a.e_stride, real).total;
   if constexpr (std::is_same<Real, float>::value) {
     // Double-buffered slots first; per-frame scales in shared memory if they
     // still fit (short utterances), else in the HBM workspace.
     FBArgs<float> b = a;
     b.sc_smem = 1;
     size_t per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad, a.T_pad,
-                              a.rep_r * a.r_stride, a.rep_e * a.e_stride, real, 2, true)
+                              pad4(a.rep_r * a.r_stride), a.rep_e * a.e_stride, real, 2, true)
                       .total;
     if (per2 > size_t(kMaxSmem) || std::getenv("LFMMI_GLOBAL_SCALES")) {
       b.sc_smem = 0;
       per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad, a.T_pad,
-                         a.rep_r * a.r_stride, a.rep_e * a.e_stride, real, 2, false)
+                         pad4(a.rep_r * a.r_stride), a.rep_e * a.e_stride, real, 2, false)
                  .total;
     }
     if (std::getenv("LFMMI_DEBUG"))
