@@ -182,11 +182,50 @@ RowEval eval_row(const int *arcs, const int *gidx, const int *pdf, const GatherL
 
 TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
                             const double *prob, const GatherLayout &gl, bool optimize) {
-  std::vector<int> order(S);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+  std::vector<int> sorted(S);
+  std::iota(sorted.begin(), sorted.end(), 0);
+  std::stable_sort(sorted.begin(), sorted.end(), [&](int x, int y) {
     return (ptr[x + 1] - ptr[x]) > (ptr[y + 1] - ptr[y]);
   });
+  // Bank-balanced tiles: a tile's 32 lanes write their states' column entries
+  // (and, backward, read alpha[state]) in one warp-wide access, conflict-free
+  // iff the states have distinct residues mod 32.  States of equal degree are
+  // interchangeable in the degree-sorted order (trips and padding unchanged),
+  // so each lane position takes an unused state of the degree it needs whose
+  // residue the tile does not hold yet, when one exists.
+  std::vector<int> order;
+  order.reserve(S);
+  if (optimize) {
+    // per degree: pool of states bucketed by residue
+    std::vector<int> deg_of(S);
+    int maxdeg = 0;
+    for (int st = 0; st < S; ++st) maxdeg = std::max(maxdeg, deg_of[st] = ptr[st + 1] - ptr[st]);
+    std::vector<std::array<std::vector<int>, 32>> pool(maxdeg + 1);
+    for (int i = S - 1; i >= 0; --i) pool[deg_of[sorted[i]]][sorted[i] & 31].push_back(sorted[i]);
+    std::vector<int> left(maxdeg + 1, 0);
+    for (int st = 0; st < S; ++st) left[deg_of[st]]++;
+    for (size_t t0 = 0; t0 < size_t(S); t0 += 32) {
+      int cnt[32] = {0};
+      const size_t t1 = std::min(size_t(S), t0 + 32);
+      for (size_t k = t0; k < t1; ++k) {
+        const int dg = deg_of[sorted[k]];  // the degree this sorted position needs
+        // least-used residue in this tile; ties -> the largest remaining pool
+        int pick = -1;
+        for (int r = 0; r < 32; ++r) {
+          if (pool[dg][r].empty()) continue;
+          if (pick < 0 || cnt[r] < cnt[pick] ||
+              (cnt[r] == cnt[pick] && pool[dg][r].size() > pool[dg][pick].size()))
+            pick = r;
+        }
+        const int st = pool[dg][pick].back();
+        pool[dg][pick].pop_back();
+        cnt[st & 31]++;
+        order.push_back(st);
+      }
+    }
+  } else {
+    order = sorted;
+  }
   const int ntiles = (S + 31) / 32;
   // Tiles are independent: schedule them in parallel into per-tile fragments
   // (each with its own RNG seed, so the result does not depend on threading).
