@@ -41,6 +41,16 @@
 
 namespace lfmmi {
 
+// cp.async pipelines, one commit group per frame: log-likelihood rows are
+// issued kTileRowAhead frames before their row maximum is taken, alpha rows
+// (backward) kTileAlphaAhead frames before use (3-slot ring, indexed mod 3), so
+// a short frame (numerators) never waits on HBM latency.
+constexpr int kTileRowAhead = 4, kTileStageRing = 8;
+constexpr int kTileAlphaAhead = 2, kTileAlphaRing = 3;
+constexpr int kTileFwdWait = kTileRowAhead - 2;   // row k+2 complete at the end of frame k
+constexpr int kTileBwdWait = kTileAlphaAhead - 1; // alpha t-2 / row t-3 at the end of frame t
+static_assert(kTileBwdWait <= kTileRowAhead - 2, "row pipeline must be at least as deep");
+
 struct TileLayout {  // byte offsets of one utterance's slice of shared memory
   size_t wp, xs, tinfo, ttrips, tbase, wlist, wtab, pdfptr, xterm, rbuf, aring, ebuf, stage,
       gstage, scales, shifts, part, mpart, total;
@@ -64,9 +74,9 @@ __host__ __device__ inline TileLayout tile_layout(bool smem_graph, int Fmax, int
   l.pdfptr = o;  o = al16(o + size_t(D + 1) * 4);
   l.xterm = o;   o = al16(o + size_t(nx) * X_pad * real); // posterior slots (nx frames)
   l.rbuf = o;    o = al16(o + size_t(2) * RB * real);     // alpha/beta columns x copies
-  l.aring = o;   o = al16(o + size_t(2) * S_pad * real);
+  l.aring = o;   o = al16(o + size_t(kTileAlphaRing) * S_pad * real);
   l.ebuf = o;    o = al16(o + size_t(2) * EB * real);     // emission rows x copies
-  l.stage = o;   o = al16(o + size_t(4) * D_pad * real);
+  l.stage = o;   o = al16(o + size_t(kTileStageRing) * D_pad * real);
   l.gstage = o;  o = al16(o + size_t(2) * D_pad * real);
   // per-frame scales / row maxima: shared memory when they fit (smem_scales),
   // else the HBM workspace (ragged, like the trellis)
@@ -268,12 +278,12 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   auto issue_row = [&](int t) {
     if (t < 0 || t >= T || cwarp >= nrw) return;
     const Real *src = Lb + size_t(t) * D;
-    Real *dst = stage + (t & 3) * D_pad;
+    Real *dst = stage + (t & (kTileStageRing - 1)) * D_pad;
     for (int d = ctid; d < D; d += GROUP) cp_async_elem(dst + d, src + d);
   };
   auto row_max_part = [&](int t) {
     if (t < 0 || t >= T || cwarp >= nrw) return;
-    const Real *src = stage + (t & 3) * D_pad;
+    const Real *src = stage + (t & (kTileStageRing - 1)) * D_pad;
     Real m = -INFINITY;
     for (int d = ctid; d < D; d += GROUP) m = nan_max(m, src[d]);
     m = warp_max(m);
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       m = lane < nrw ? mp[lane] : Real(-INFINITY);
       m = warp_max(m);
     }
-    const Real *src = stage + (t & 3) * D_pad;
+    const Real *src = stage + (t & (kTileStageRing - 1)) * D_pad;
     Real *dst = ebuf + (t & 1) * EB;
     for (int d = ctid; d < D; d += GROUP) {
       const Real v = exp_r(src[d] - m);
@@ -310,10 +320,11 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   for (int i = tid; i < 2 * RB; i += GROUP) rbuf[i] = Real(0);  // padding lanes stay 0
   gsync();
   for (int s = tid; s < S; s += GROUP) put_vec(rbuf, s, (s == init) ? Real(1) : Real(0));
-  issue_row(0);
-  issue_row(1);
-  cp_async_commit();
-  cp_async_wait<0>();
+  for (int j = 0; j < kTileRowAhead; ++j) {  // group j holds row j (+ the staged packs in 0)
+    issue_row(j);
+    cp_async_commit();
+  }
+  cp_async_wait<kTileFwdWait>();
   row_max_part(0);
   row_max_part(1);
   gsync();
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       }
     }
     if (k + 1 < T) compute_e(k + 1, true);
-    issue_row(k + 2);
+    issue_row(k + kTileRowAhead);
     cp_async_commit();
     {
       const Real *e = ebuf + cur * EB;
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       psum = warp_sum(psum);
       if (lane == 0) part[nxt * 32 + warp] = psum;
     }
-    cp_async_wait<0>();
+    cp_async_wait<kTileFwdWait>();  // row k + 2
     row_max_part(k + 2);
     gsync();
   }
@@ -482,7 +493,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   }
   auto issue_alpha = [&](int k) {
     if (k < 0) return;
-    copy16<GROUP>(aring + (k & 1) * S_pad, trellis + size_t(k) * S_pad,
+    copy16<GROUP>(aring + (k % kTileAlphaRing) * S_pad, trellis + size_t(k) * S_pad,
                   size_t(S_pad) * sizeof(Real), ctid);
   };
   auto issue_post = [&](int t) {
@@ -523,10 +534,15 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   };
 
   for (int s = tid; s < S; s += GROUP) put_vec(rbuf + (T & 1) * RB, s, fin[s] * (Real(1) + lam));
-  issue_row(T - 1);
-  issue_row(T - 2);
-  issue_alpha(T - 1);
-  cp_async_commit();
+  // Backward pipeline: "iteration" u issues row u-1-kTileRowAhead, alpha
+  // u-1-kTileAlphaAhead (and, ADD/SUBTRACT modes, gradient row u-1); the virtual
+  // iterations T+kTileRowAhead .. T+1 fill it, one group each.
+  for (int u = T + kTileRowAhead; u > T; --u) {
+    if (u - 1 - kTileRowAhead < T) issue_row(u - 1 - kTileRowAhead);
+    if (u - 1 - kTileAlphaAhead < T) issue_alpha(u - 1 - kTileAlphaAhead);
+    if (u - 1 < T) issue_post(u - 1);
+    cp_async_commit();
+  }
   cp_async_wait<0>();
   row_max_part(T - 1);
   row_max_part(T - 2);
@@ -548,14 +564,14 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     const int xb = XDB ? ct : 0;
     if (XDB && t < T && flusher) flush_post(t, xterm + (xb ^ 1) * X_pad);
     if (t - 2 >= 0) compute_e(t - 2, false);
-    issue_row(t - 3);
-    issue_alpha(t - 2);
+    issue_row(t - 1 - kTileRowAhead);
+    issue_alpha(t - 1 - kTileAlphaAhead);
     issue_post(t - 1);
     cp_async_commit();
     {
       const Real *bt = rbuf + ct * RB;
       const Real *e = ebuf + cp * EB;
-      const Real *al = aring + cp * S_pad;  // alpha_{t-1}
+      const Real *al = aring + ((t - 1) % kTileAlphaRing) * S_pad;  // alpha_{t-1}
       Real *bn = rbuf + cp * RB;
       Real *xt = xterm + xb * X_pad;
       Real dp = Real(0);
@@ -591,7 +607,10 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
       dp = warp_sum(dp);
       if (lane == 0) part[cp * 32 + warp] = dp;
     }
-    cp_async_wait<0>();
+    if (reads_post)
+      cp_async_wait<0>();  // the gradient row read by the next flush is this group's
+    else
+      cp_async_wait<kTileBwdWait>();  // alpha t-2 and row t-3
     row_max_part(t - 3);
     gsync();
     if (!XDB) {
