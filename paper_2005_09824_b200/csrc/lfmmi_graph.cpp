@@ -333,6 +333,11 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           int spl = 1;
           while (spl < 32 && num_pdfs * spl * 2 <= 32 * kTableNW) spl <<= 1;
           const int lanes = num_pdfs * spl;
+          static const int chore_bias_bwd = [] {  // LFMMI_CHORE_BIAS_BWD overrides (A/B)
+            const char *e = std::getenv("LFMMI_CHORE_BIAS_BWD");
+            return e ? std::atoi(e) : chore_bias;
+          }();
+          for (int w = kTableNW - chore; w < kTableNW; ++w) bias[w] = chore_bias_bwd;
           if (lanes < 32 * kTableNW && !std::getenv("LFMMI_NO_FLUSH_BIAS")) {
             const int fw = (lanes + 31) / 32;
             const int per_lane = (xpad / 4 + lanes - 1) / lanes;
