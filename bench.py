@@ -285,6 +285,7 @@ def run_ours(args):
     # (default): the denominator pass, the step's critical path (the numerator
     # pass runs concurrently on an auxiliary stream; combine + totals ~15 us).
     launches_per_step = int(ext.last_launch_count())
+    den_kernel = str(ext.last_den_kernel())
     fused = launches_per_step == 1
 
     def dominant_launch():
@@ -406,8 +407,7 @@ def run_ours(args):
                        "parallelism": f"dp{world} (sequence-sharded, scalar all-reduce)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("fb_chain_kernel<512> (num+den+grad, one launch)" if fused
-                                    else "fb_tile_kernel<float,512,1,1,0> (denominator pass)"),
+                         "kernel": den_kernel,
                          "algorithmic_bytes_per_launch": A, "launch_ms": kernel_ms,
                          "algorithmic_bytes_per_step": A_step,
                          "peak_source": peak_src},

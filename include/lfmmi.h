@@ -57,6 +57,13 @@ const char *lfmmi_version(void);
 int32_t lfmmi_last_launch_count(void);
 
 /*
+ * Name of the kernel that ran the last denominator-sized (one CTA or cluster
+ * per utterance) forward-backward on this thread, e.g. "fb_split_kernel".
+ * Diagnostic (benchmarks label their roofline line with it).
+ */
+const char *lfmmi_last_den_kernel(void);
+
+/*
  * Build a device-resident graph batch from the reference's padded host
  * layout (graph.py:253-279).  G physical rows; row r has row_num_states[r]
  * states and row_num_arcs[r] arcs.  Arrays are (G, max_arcs) in the

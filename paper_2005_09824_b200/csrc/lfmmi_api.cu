@@ -283,6 +283,7 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
     const int rc = launch_stream<Real>(a, graphs, st);
     if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
   }
+  if (!small) note_den_kernel("fb_group_kernel<1024>");
   return launch_group<Real>(a, small ? choose_group(graphs->max_states) : 1024, st);
 }
 
@@ -438,6 +439,12 @@ AuxStream &aux_for_device() {
 }  // namespace
 
 extern "C" int32_t lfmmi_last_launch_count(void) { return g_launches; }
+
+namespace {
+thread_local const char *g_den_kernel = "";
+}
+void lfmmi::note_den_kernel(const char *name) { g_den_kernel = name; }
+extern "C" const char *lfmmi_last_den_kernel(void) { return g_den_kernel; }
 
 static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_row_map,
                                 const lfmmi_graphs *denominator, const int64_t *den_row_map,

@@ -737,6 +737,7 @@ static int launch_profiled(const ChainArgs &a0, const ChainDims &m, const ChainL
 }
 
 int launch_chain(const ChainArgs &a, const ChainDims &m, cudaStream_t st) {
+  note_den_kernel("fb_chain_kernel<512> (num+den+grad, one launch)");
   const int RBd = pad4(a.rep_rd * a.r_strided), RBn = pad4(a.rep_rn * a.r_striden),
             EB = a.rep_e * a.e_stride;
   const ChainLayout l2 =

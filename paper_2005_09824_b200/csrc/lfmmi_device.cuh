@@ -105,6 +105,7 @@ struct FBArgs {
   long long sc_off;    // tile kernel: per-frame scales at work + sc_off + item_off,
   long long sc_total;  //   row maxima sc_total Reals further (ragged, like the trellis)
   int sc_smem;         //   ... or in shared memory (1; set by the launcher when they fit)
+  long long *prof;     // split kernel debug timestamps (LFMMI_PROFILE_SPLIT), normally NULL
 };
 
 }  // namespace lfmmi

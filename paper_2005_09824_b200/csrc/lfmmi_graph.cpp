@@ -63,12 +63,12 @@ struct HostPack {
   std::vector<double> fin64;
   std::vector<unsigned> tf_info, tb_info, tf_word, tb_word;
   std::vector<int> tf_trips, tf_base, tb_trips, tb_base, pdf_arc_ptr;
-  std::vector<int> tf_wlist, tb_wlist, tf_wtab, tb_wtab;
+  std::vector<int> tf_wlist, tb_wlist, tf_wtab, tb_wtab, tp_wlist, tp_wtab;
   std::vector<int> sf_info, sb_info, sf_trips, sf_base, sb_trips, sb_base;
   std::vector<uint2> sf_wp, sb_wp;
   std::vector<float> tf_p32, tb_p32;
   std::vector<double> tf_p64, tb_p64;
-  std::vector<unsigned short> tb_xslot;
+  std::vector<unsigned short> tb_xslot, tf_xslot;
   std::vector<uint2> tf_wp, tb_wp;
 };
 
@@ -301,7 +301,13 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
       std::vector<int> pptr, xslot;
       int xpad = 0;
       assign_xslots(tb, &h.out_pdf[a0], num_pdfs, I, 4, pptr, xslot, xpad);
-      tileable = xpad <= 65536;
+      // Forward-pack posterior slots (fb_split_kernel: the forward CTA writes the
+      // posteriors of the second half of the utterance).  The per-pdf slot
+      // groups depend only on the pdf counts, so both packs share pdf_arc_ptr.
+      std::vector<int> pptr_f, xslot_f;
+      int xpad_f = 0;
+      assign_xslots(tf, &h.in_pdf[a0], num_pdfs, I, 4, pptr_f, xslot_f, xpad_f);
+      tileable = xpad <= 65536 && pptr_f == pptr && xpad_f == xpad;
       if (tileable) {
         d[kXPad] = xpad;
         h.pdf_arc_ptr.insert(h.pdf_arc_ptr.end(), pptr.begin(), pptr.end());
@@ -351,11 +357,17 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           warp_lists(tb.trips, bias, tab, lst);
           h.tb_wtab.insert(h.tb_wtab.end(), tab.begin(), tab.end());
           h.tb_wlist.insert(h.tb_wlist.end(), lst.begin(), lst.end());
+          // forward with posteriors (fb_split_kernel, second half): same chores as
+          // the backward (emission row + gradient-row flush)
+          warp_lists(tf.trips, bias, tab, lst);
+          h.tp_wtab.insert(h.tp_wtab.end(), tab.begin(), tab.end());
+          h.tp_wlist.insert(h.tp_wlist.end(), lst.begin(), lst.end());
         }
         h.tf_info.insert(h.tf_info.end(), tf.info.begin(), tf.info.end());
         h.tb_info.insert(h.tb_info.end(), tb.info.begin(), tb.info.end());
         while (h.tf_trips.size() % 4) {  // keep per-row tile arrays 16-byte aligned
           h.tf_wlist.push_back(0);
+          h.tp_wlist.push_back(0);
           h.tb_wlist.push_back(0);
           h.tf_trips.push_back(0);
           h.tf_base.push_back(0);
@@ -387,6 +399,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           h.tb_p32.push_back(float(p));
         }
         for (int x : xslot) h.tb_xslot.push_back((unsigned short)x);
+        for (int x : xslot_f) h.tf_xslot.push_back((unsigned short)x);
         max_xpad = std::max(max_xpad, xpad);
         d[kTfSlots] = int(tf.word_idx.size());
         d[kTbSlots] = int(tb.word_idx.size());
@@ -465,6 +478,8 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   add(h.sf_wp, &dv.sf_wp);
   add(h.sb_wp, &dv.sb_wp);
   add(h.tf_wlist, &dv.tf_wlist);
+  add(h.tp_wlist, &dv.tp_wlist);
+  add(h.tp_wtab, &dv.tp_wtab);
   add(h.tb_wlist, &dv.tb_wlist);
   add(h.tf_wtab, &dv.tf_wtab);
   add(h.tb_wtab, &dv.tb_wtab);
@@ -478,6 +493,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   add(h.tf_p64, &dv.tf_p64);
   add(h.tb_p64, &dv.tb_p64);
   add(h.tb_xslot, &dv.tb_xslot);
+  add(h.tf_xslot, &dv.tf_xslot);
   add(h.pdf_arc_ptr, &dv.pdf_arc_ptr);
   add(h.tf_wp, &dv.tf_wp);
   add(h.tb_wp, &dv.tb_wp);

@@ -66,10 +66,12 @@ struct DevGraphs {
   const int *tf_trips, *tf_base, *tb_trips, *tb_base;
   const int *tf_wlist, *tb_wlist;     // tile ids grouped by warp (16-warp LPT schedule)
   const int *tf_wtab, *tb_wtab;       // per-warp ranges + warps by ascending load
+  const int *tp_wlist, *tp_wtab;      // forward lists with flush chores (split kernel)
   const unsigned *tf_word, *tb_word;  // src|pdf<<16 (forward), dst|pdf<<16 (backward)
   const float *tf_p32, *tb_p32;
   const double *tf_p64, *tb_p64;
   const unsigned short *tb_xslot;     // posterior slot of each backward arc
+  const unsigned short *tf_xslot;     // ... of each forward arc (same slot groups)
   const int *pdf_arc_ptr;             // posterior slot range per pdf (16-byte aligned)
   const uint2 *tf_wp, *tb_wp;         // interleaved (word, fp32 prob bits) slots
   const int *sf_info, *sb_info;       // stream packs: state per tile lane (-1 = none)
@@ -95,4 +97,6 @@ struct lfmmi_graphs {
 namespace lfmmi {
 int set_error(int code, const std::string &msg);
 int check_cuda(cudaError_t err, const char *what);
+// Records the kernel of the last denominator-sized launch (lfmmi_last_den_kernel).
+void note_den_kernel(const char *name);
 }  // namespace lfmmi

@@ -22,6 +22,12 @@ template <typename Real>
 int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *graphs, bool warp_per_item,
                 cudaStream_t st);
 
+// Denominator forward-backward split over a 2-CTA cluster (forward CTA +
+// backward CTA meeting at the midpoint; lfmmi_split.cu).  fp32, uniform leak,
+// WRITE / NEGATE; LFMMI_ERR_UNSUPPORTED (without launching) when not applicable.
+template <typename Real>
+int launch_split(const FBArgs<Real> &a, const lfmmi_graphs *graphs, cudaStream_t st);
+
 // L2-streamed forward-backward for graphs too large for the on-chip packs
 // (lfmmi_stream.cu; fp32, uniform leak, WRITE/NEGATE).  LFMMI_ERR_UNSUPPORTED
 // (without launching) when not applicable.

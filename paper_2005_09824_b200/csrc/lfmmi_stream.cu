@@ -462,6 +462,9 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
   const char *env = std::getenv("LFMMI_STREAM_MODE");  // "1024x1", "1024x2", "512x2"
   std::string mode = env ? env : (2 * a.B <= sms ? "1024x2" : "1024x1");
+  note_den_kernel(mode == "1024x2"  ? "fb_stream_kernel<1024,2>"
+                  : mode == "512x2" ? "fb_stream_kernel<512,2>"
+                                    : "fb_stream_kernel<1024,1>");
   if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, S32, lay, st);
   if (mode == "512x2") return launch_stream_impl<512, 2>(a, S32, lay, st);
   return launch_stream_impl<1024, 1>(a, S32, lay, st);

@@ -688,6 +688,10 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
   const size_t per = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
                                  a.T_pad, pad4(a.rep_r * a.r_stride), a.rep_e * a.e_stride, real).total;
   if constexpr (std::is_same<Real, float>::value) {
+    // Fewer utterances than ~2x SMs: forward and backward of each utterance on
+    // two SMs (cluster), load-balanced over the batch (lfmmi_split.cu).
+    const int rc = launch_split<float>(a, g, st);
+    if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
     // Double-buffered slots first; per-frame scales in shared memory if they
     // still fit (short utterances), else in the HBM workspace.
     FBArgs<float> b = a;
@@ -704,12 +708,15 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     if (std::getenv("LFMMI_DEBUG"))
       std::fprintf(stderr, "[lfmmi] den tile smem single=%zu double=%zu limit=%d\n", per, per2,
                    kMaxSmem);
-    if (!a.leak_pi && per2 <= size_t(kMaxSmem) && !std::getenv("LFMMI_TILE_SINGLE_X"))
+    if (!a.leak_pi && per2 <= size_t(kMaxSmem) && !std::getenv("LFMMI_TILE_SINGLE_X")) {
+      note_den_kernel("fb_tile_kernel<float,512,1,1,0,1> (XDB)");
       return launch_tile_impl2<float, kDenGroup, 1, true, false, true>(b, g, per2, st);
+    }
   }
   if (per > size_t(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "tile pack needs " + std::to_string(per) + " B shared memory");
+  note_den_kernel("fb_tile_kernel<Real,512,1,1,*> (single slot buffer)");
   return launch_tile_impl<Real, kDenGroup, 1, true>(a, g, per, st);
 }
 

@@ -192,4 +192,89 @@ __device__ __forceinline__ float bwd_tile_f32(uint32_t sb, uint32_t xb, int trip
   return A;
 }
 
+// Forward arc sums with posterior slots (fb_split_kernel, second half of the
+// forward CTA): term = p e[pdf] (r[src] + lu); A = sum term; slot xs <- cb * term
+// (cb = beta(dst) / scale, one value per lane).
+__device__ __forceinline__ float fwd_post_tile_f32(uint32_t sb, uint32_t xb, int trips,
+                                                   uint32_t e32, uint32_t r32, uint32_t x32,
+                                                   float lu, float cb) {
+  float A = 0.f;
+  int j = 0;
+#pragma unroll 1
+  for (; j + 4 <= trips; j += 4, sb += 4 * 256, xb += 4 * 64) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
+                w3 = lds_v2(sb + 768);
+    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64), x2 = lds_h(xb + 128),
+                   x3 = lds_h(xb + 192);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
+                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
+    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu)),
+                r2 = lds_f(r32 + (w2.x & 0xFFFFu)), r3 = lds_f(r32 + (w3.x & 0xFFFFu));
+    const float t0 = __uint_as_float(w0.y) * e0 * (r0 + lu),
+                t1 = __uint_as_float(w1.y) * e1 * (r1 + lu),
+                t2 = __uint_as_float(w2.y) * e2 * (r2 + lu),
+                t3 = __uint_as_float(w3.y) * e3 * (r3 + lu);
+    A += (t0 + t1) + (t2 + t3);
+    sts_f(x32 + 4 * x0, cb * t0);
+    sts_f(x32 + 4 * x1, cb * t1);
+    sts_f(x32 + 4 * x2, cb * t2);
+    sts_f(x32 + 4 * x3, cb * t3);
+  }
+  if (j + 2 <= trips) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
+    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
+    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu));
+    const float t0 = __uint_as_float(w0.y) * e0 * (r0 + lu),
+                t1 = __uint_as_float(w1.y) * e1 * (r1 + lu);
+    A += t0 + t1;
+    sts_f(x32 + 4 * x0, cb * t0);
+    sts_f(x32 + 4 * x1, cb * t1);
+    j += 2;
+    sb += 2 * 256;
+    xb += 2 * 64;
+  }
+  if (j < trips) {
+    const uint2 w = lds_v2(sb);
+    const uint32_t x = lds_h(xb);
+    const float t = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16)) *
+                    (lds_f(r32 + (w.x & 0xFFFFu)) + lu);
+    A += t;
+    sts_f(x32 + 4 * x, cb * t);
+  }
+  return A;
+}
+
+// Backward arc sums without posterior slots (fb_split_kernel, first half of the
+// backward CTA): A = sum p e[pdf] (b[dst] + ld).
+__device__ __forceinline__ float bwd_plain_tile_f32(uint32_t sb, int trips, uint32_t e32,
+                                                    uint32_t b32, float ld) {
+  float A = 0.f;
+  int j = 0;
+#pragma unroll 1
+  for (; j + 4 <= trips; j += 4, sb += 4 * 256) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
+                w3 = lds_v2(sb + 768);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
+                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
+    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu)),
+                b2 = lds_f(b32 + (w2.x & 0xFFFFu)), b3 = lds_f(b32 + (w3.x & 0xFFFFu));
+    A += (__uint_as_float(w0.y) * e0 * (b0 + ld) + __uint_as_float(w1.y) * e1 * (b1 + ld)) +
+         (__uint_as_float(w2.y) * e2 * (b2 + ld) + __uint_as_float(w3.y) * e3 * (b3 + ld));
+  }
+  if (j + 2 <= trips) {
+    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
+    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
+    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu));
+    A += __uint_as_float(w0.y) * e0 * (b0 + ld) + __uint_as_float(w1.y) * e1 * (b1 + ld);
+    j += 2;
+    sb += 2 * 256;
+  }
+  if (j < trips) {
+    const uint2 w = lds_v2(sb);
+    A += __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16)) * (lds_f(b32 + (w.x & 0xFFFFu)) + ld);
+  }
+  return A;
+}
+
 }  // namespace lfmmi

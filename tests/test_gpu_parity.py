@@ -116,11 +116,22 @@ def test_three_phase_api(cuda, name):
 
 
 # ------------------------------------------------- BASELINE configs vs oracle
-@pytest.mark.parametrize("kernel", ["auto", "tile1x", "fused", "fused1x", "group"])
+def _kernel_env(kernel, monkeypatch):
+    """Denominator kernel selection shared by the parity tests."""
+    if kernel == "tile":  # one CTA per utterance (no forward/backward split)
+        monkeypatch.setenv("LFMMI_SPLIT", "0")
+    if kernel in ("split1", "split2"):  # 2-CTA split, several utterances per cluster
+        monkeypatch.setenv("LFMMI_SPLIT", "1")
+        monkeypatch.setenv("LFMMI_SPLIT_CLUSTERS", kernel[-1])
+
+
+@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "fused", "fused1x",
+                                    "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])
 def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
+    _kernel_env(kernel, monkeypatch)
     if kernel == "tile1x":  # denominator tile kernel with a single posterior slot buffer
         monkeypatch.setenv("LFMMI_TILE_SINGLE_X", "1")
     if kernel in ("fused", "fused1x"):  # single-launch num+den+grad kernel (opt-in)
@@ -236,14 +247,18 @@ def test_failure_semantics(cuda):
     assert math.isnan(num_lp) and not math.isnan(den_lp)
 
 
+@pytest.mark.parametrize("late", [False, True])
 @pytest.mark.parametrize("config,batch_size,kernel", [
-    ("wsj_mono", 4, "auto"), ("wsj_mono", 4, "tile1x"), ("wsj_mono", 4, "fused"),
+    ("wsj_mono", 4, "auto"), ("wsj_mono", 4, "tile"), ("wsj_mono", 4, "split1"),
+    ("wsj_mono", 4, "tile1x"), ("wsj_mono", 4, "fused"),
     ("wsj_biphone", 3, "auto"), ("large", 2, "auto"), ("large", 2, "stream1")])
-def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kernel, monkeypatch):
+def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kernel, late,
+                                                  monkeypatch):
     """A NaN log-likelihood makes that utterance's column totals NaN -> it fails
     at that frame in both graphs (_kernels.py:114-118); the others are untouched
     and chain_loss excludes it (loss.py:61-69).  Covers the early-exit paths of
     the XDB tile kernel, the fused kernel and the 1- and 2-CTA stream kernel."""
+    _kernel_env(kernel, monkeypatch)
     if kernel == "tile1x":
         monkeypatch.setenv("LFMMI_TILE_SINGLE_X", "1")
     if kernel == "fused":
@@ -254,7 +269,9 @@ def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kern
     batch, nums, den = w.build(P)  # make_batch rejects non-finite input: poison afterwards
     bad = 1
     values = np.array(batch.values)
-    values[bad, 5, 3] = np.nan
+    # early frame, or one after the split kernel's midpoint (forward CTA already
+    # writing posteriors, backward CTA past the barrier)
+    values[bad, int(batch.lengths[bad]) - 3 if late else 5, 3] = np.nan
     batch = P.LogLikBatch(values=values, lengths=batch.lengths,
                           valid_batch_sizes=batch.valid_batch_sizes, order_map=batch.order_map)
     res = P.chain_loss(batch, nums, den)
@@ -281,6 +298,40 @@ def test_stream_kernel_short_utterances(cuda, mode, monkeypatch):
     rf = O.forward_backward(batch, den, leak=1e-5)
     np.testing.assert_allclose(fb.log_probs, rf.log_probs, rtol=1e-6, atol=1e-6)
     assert np.abs(fb.posteriors - rf.posteriors).max() <= FP32_GRAD_ABS
+
+
+@pytest.mark.parametrize("kernel", ["tile", "split1", "split2"])
+def test_split_kernel_short_and_odd_utterances(cuda, kernel, monkeypatch):
+    """1, 2, 3, 4, 7 and 300-frame utterances through the denominator tile kernels:
+    midpoint h = T/2 at 0 (no backward posterior frames), odd T, and several
+    utterances per cluster (split1: all in one cluster, pack bound once)."""
+    _kernel_env(kernel, monkeypatch)
+    w = synth.make_workload("wsj_mono", seed=10, batch_size=6)
+    rng = np.random.default_rng(0)
+    seqs = [rng.normal(0, 2, (t, w.D)).astype(np.float32).astype(np.float64)
+            for t in (1, 2, 3, 4, 7, 300)]
+    batch = P.make_batch(seqs)
+    den = P.ChainGraphBatch.broadcast(w.den_graph(P), 6)
+    fb = P.forward_backward(batch, den)
+    rf = O.forward_backward(batch, den, leak=1e-5)
+    np.testing.assert_allclose(fb.log_probs, rf.log_probs, rtol=1e-6, atol=1e-6)
+    assert np.abs(fb.posteriors - rf.posteriors).max() <= FP32_GRAD_ABS
+
+
+@pytest.mark.parametrize("kernel", ["tile", "split2"])
+def test_split_kernel_bitwise_batch_independent(cuda, kernel, monkeypatch):
+    """An utterance's result does not depend on its batch-mates or on which
+    cluster / position in a cluster's list it lands (fixed reduction orders)."""
+    _kernel_env(kernel, monkeypatch)
+    w = synth.make_workload("wsj_mono", seed=11, batch_size=8)
+    batch, nums, den = w.build(P)
+    full = P.forward_backward(batch, den)
+    sub = P.make_batch([batch.values[b, :batch.lengths[b]] for b in (2, 5)])
+    part = P.forward_backward(sub, P.ChainGraphBatch.broadcast(den.graph(0), 2))
+    for i, b in enumerate((2, 5)):
+        assert full.log_probs[b] == part.log_probs[i]
+        np.testing.assert_array_equal(full.posteriors[b, :batch.lengths[b]],
+                                      part.posteriors[i, :batch.lengths[b]])
 
 
 def test_custom_leak_distribution(cuda):
@@ -349,7 +400,7 @@ def test_numerator_group_sizes(cuda, num_group, monkeypatch):
     assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
 
 
-@pytest.mark.parametrize("kernel", ["auto", "fused", "stream"])
+@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "fused", "stream"])
 @pytest.mark.parametrize("config,batch_size", [("wsj_mono", 7), ("sweep", 5),
                                                ("wsj_biphone", 3), ("large", 2)])
 def test_packed_ragged_batch_any_order(cuda, config, batch_size, kernel, monkeypatch):
@@ -357,6 +408,7 @@ def test_packed_ragged_batch_any_order(cuda, config, batch_size, kernel, monkeyp
     no padding; grad comes back in the same ragged layout."""
     import torch
 
+    _kernel_env(kernel, monkeypatch)
     if kernel == "fused":
         monkeypatch.setenv("LFMMI_FUSED", "1")
     if kernel == "stream" and config not in ("wsj_biphone", "large"):
