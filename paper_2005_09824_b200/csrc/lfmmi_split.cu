@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 namespace cg = cooperative_groups;
@@ -344,8 +345,10 @@ __global__ void __launch_bounds__(kNT, 1)
 
       float inv2 = 1.f, leakc = 0.f;
       int fail_at = -1;
-      stamp(1);
-      for (int k = 0; k < T; ++k) {
+      // One forward frame; POST (compile-time) adds the posterior slots.  Returns
+      // false when the frame's input column fails the scale floor.
+      auto fframe = [&](int k, auto postc) -> bool {
+        constexpr bool POST = decltype(postc)::value;
         const int cur = k & 1, nxt = cur ^ 1;
         if (k > 0) {
           const float t0 = lane_sum<kNW>(part + cur * 32, lane);
@@ -357,28 +360,10 @@ __global__ void __launch_bounds__(kNT, 1)
           }
           if (!(t2 >= a.floor_eff) || isinf(t2)) {
             fail_at = k - 1;
-            break;
+            return false;
           }
           inv2 = rcp_rn(t2);
           if (tid == 0) scales[k - 1] = t2;
-        }
-        const bool post = k >= h && !other_failed;
-        if (k == h) {
-          stamp(2);
-          cluster_barrier();
-          mid_done = true;
-          if (post) {
-            for (int q = 0; q < kRingAhead; ++q) issue_trellis(h + q);
-            cp_async_commit();
-            cp_async_wait<0>();
-            __syncthreads();
-          }
-          stamp(3);
-          if (post) {
-            wl = wl2;
-            wlo = wt2[warp];
-            whi = wt2[warp + 1];
-          }
         }
         const float lu = leakc * upi;
         if (k < h) {  // alpha'_{k-1} for the backward CTA's posteriors
@@ -393,18 +378,16 @@ __global__ void __launch_bounds__(kNT, 1)
             a4[q] = v;
           }
         }
-        if (post && k - 1 >= h && flusher)
+        if (POST && k - 1 >= h && flusher)
           flush_post(k - 1, xterm + ((k - 1) & 1) * X_pad,
                      rcp_rn(lane_sum<kNW>(partz + ((k - 1) & 1) * 32, lane)));
         if (k + 1 < T) compute_e(k + 1, true);
         issue_row(k + kRowAhead);
-        if (post) issue_trellis(k + kRingAhead);
+        if (POST) issue_trellis(k + kRingAhead);
         cp_async_commit();
         {
           const uint32_t e32 = smem_u32(ebuf + cur * EB), r32 = smem_u32(rbuf + cur * RB);
           float *rn = rbuf + nxt * RB;
-          const float *bet = ring + (k % kRing) * S_pad;
-          const uint32_t x32 = smem_u32(xterm + (k & 1) * X_pad);
           const bool last = (k + 1 == T);
           float psum = 0.f, zp = 0.f;
           for (int rr = wlo; rr < whi; ++rr) {
@@ -414,11 +397,12 @@ __global__ void __launch_bounds__(kNT, 1)
             const int base = tbase[tile] + lane;
             const int s = int(info & 0xFFFFu);
             float raw;
-            if (post) {
+            if constexpr (POST) {
+              const float *bet = ring + (k % kRing) * S_pad;
               const float cb = s != 0xFFFF ? inv2 * bet[s] : 0.f;
               const float A = fwd_post_tile_f32(wp32 + uint32_t(base) * 8u,
                                                 xs32 + uint32_t(base) * 2u, trips, e32, r32,
-                                                x32, lu, cb);
+                                                smem_u32(xterm + (k & 1) * X_pad), lu, cb);
               raw = inv2 * A;
               zp = fmaf(cb, A, zp);
             } else {
@@ -437,14 +421,42 @@ __global__ void __launch_bounds__(kNT, 1)
           }
           psum = warp_sum(psum);
           if (lane == 0) part[nxt * 32 + warp] = psum;
-          if (post) {
+          if constexpr (POST) {
             zp = warp_sum(zp);
             if (lane == 0) partz[(k & 1) * 32 + warp] = zp;
           }
         }
-        cp_async_wait<kWait>();
+        // plain frames: log-likelihood rows only, two frames of slack; posterior
+        // frames: the trellis row issued last frame must land too
+        if constexpr (POST)
+          cp_async_wait<kWait>();
+        else
+          cp_async_wait<kRowAhead - 2>();
         row_max_part(k + 2);
         __syncthreads();
+        return true;
+      };
+      stamp(1);
+      bool ok = true;
+      for (int k = 0; k < h && ok; ++k) ok = fframe(k, std::false_type{});
+      if (ok) {
+        stamp(2);
+        cluster_barrier();
+        mid_done = true;
+        if (!other_failed) {
+          for (int q = 0; q < kRingAhead; ++q) issue_trellis(h + q);
+          cp_async_commit();
+          cp_async_wait<0>();
+          __syncthreads();
+          wl = wl2;
+          wlo = wt2[warp];
+          whi = wt2[warp + 1];
+        }
+        stamp(3);
+        if (!other_failed)
+          for (int k = h; k < T && ok; ++k) ok = fframe(k, std::true_type{});
+        else
+          for (int k = h; k < T && ok; ++k) ok = fframe(k, std::false_type{});
       }
       if (fail_at < 0) {
         const float t0 = lane_sum<kNW>(part + (T & 1) * 32, lane);
@@ -521,26 +533,15 @@ __global__ void __launch_bounds__(kNT, 1)
         __syncthreads();
 
         // iteration t: arcs of frame f = t-1; beta column "t" (raw) in rbuf[t & 1]
-        stamp(1);
-        for (int t = T; t >= 1; --t) {
+        auto bframe = [&](int t, auto postc) {
+          constexpr bool POST = decltype(postc)::value;
           const int ct = t & 1, cpar = ct ^ 1;
           const int f = t - 1;
-          const bool post = f < h;
-          if (t == h) {  // first posterior frame: the forward CTA's alpha rows are final
-            stamp(2);
-            cluster_barrier();
-            mid_done = true;
-            for (int q = 0; q < kRingAhead; ++q) issue_trellis(f - q);
-            cp_async_commit();
-            cp_async_wait<0>();
-            __syncthreads();
-            stamp(3);
-          }
           const float t0 = lane_sum<kNW>(part + ct * 32, lane);  // mean of the raw column
           const float ld = (t < T && lam > 0.f) ? lam * t0 : 0.f;
           const float n = float(S) * t0;
           const float inv = (n > 0.f && !isinf(n)) ? rcp_rn(n) : 1.f;
-          if (!post) {  // beta'_f for the forward CTA's posteriors
+          if constexpr (!POST) {  // beta'_f for the forward CTA's posteriors
             const float4 *r4 = reinterpret_cast<const float4 *>(rbuf + ct * RB);
             float4 *b4 = reinterpret_cast<float4 *>(trellis + size_t(f) * S_pad);
             for (int q = tid; q < (S_pad >> 2); q += kNT) {
@@ -552,18 +553,16 @@ __global__ void __launch_bounds__(kNT, 1)
               b4[q] = v;
             }
           }
-          if (t < h && flusher)  // frame t (posterior, previous iteration)
+          if (POST && t < h && flusher)  // frame t (posterior, previous iteration)
             flush_post(t, xterm + (t & 1) * X_pad,
                        rcp_rn(lane_sum<kNW>(partz + (t & 1) * 32, lane)));
           if (t - 2 >= 0) compute_e(t - 2, false);
           issue_row(t - 1 - kRowAhead);
-          if (post) issue_trellis(f - kRingAhead);
+          if (POST) issue_trellis(f - kRingAhead);
           cp_async_commit();
           {
             const uint32_t e32 = smem_u32(ebuf + cpar * EB), b32 = smem_u32(rbuf + ct * RB);
-            const float *al = ring + (f % kRing) * S_pad;  // alpha'_{f-1} = trellis row f
             float *bn = rbuf + cpar * RB;
-            const uint32_t x32 = smem_u32(xterm + (f & 1) * X_pad);
             float dq = 0.f, zp = 0.f;
             for (int rr = wlo; rr < whi; ++rr) {
               const int tile = wl[rr];
@@ -572,10 +571,11 @@ __global__ void __launch_bounds__(kNT, 1)
               const int base = tbase[tile] + lane;
               const int s = int(info & 0xFFFFu);
               float A;
-              if (post) {
+              if constexpr (POST) {
+                const float *al = ring + (f % kRing) * S_pad;  // alpha'_{f-1} = trellis row f
                 const float as = s != 0xFFFF ? al[s] : 0.f;
                 A = bwd_tile_f32(wp32 + uint32_t(base) * 8u, xs32 + uint32_t(base) * 2u, trips,
-                                 e32, b32, x32, ld, as);
+                                 e32, b32, smem_u32(xterm + (f & 1) * X_pad), ld, as);
                 zp = fmaf(as, A, zp);
               } else {
                 A = bwd_plain_tile_f32(wp32 + uint32_t(base) * 8u, trips, e32, b32, ld);
@@ -588,14 +588,30 @@ __global__ void __launch_bounds__(kNT, 1)
             }
             dq = warp_sum(dq);
             if (lane == 0) part[cpar * 32 + warp] = dq;
-            if (post) {
+            if constexpr (POST) {
               zp = warp_sum(zp);
               if (lane == 0) partz[(f & 1) * 32 + warp] = zp;
             }
           }
-          cp_async_wait<kWait>();
+          if constexpr (POST)
+            cp_async_wait<kWait>();
+          else
+            cp_async_wait<kRowAhead - 2>();
           row_max_part(t - 3);
           __syncthreads();
+        };
+        stamp(1);
+        for (int t = T; t > h; --t) bframe(t, std::false_type{});
+        if (h >= 1) {  // first posterior frame h-1: the forward CTA's alpha rows are final
+          stamp(2);
+          cluster_barrier();
+          mid_done = true;
+          for (int q = 0; q < kRingAhead; ++q) issue_trellis(h - 1 - q);
+          cp_async_commit();
+          cp_async_wait<0>();
+          __syncthreads();
+          stamp(3);
+          for (int t = h; t >= 1; --t) bframe(t, std::true_type{});
         }
         if (h >= 1 && flusher)
           flush_post(0, xterm, rcp_rn(lane_sum<kNW>(partz, lane)));

@@ -38,6 +38,7 @@
 #include <cstdlib>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 namespace lfmmi {
 
@@ -50,6 +51,14 @@ constexpr int kTileAlphaAhead = 2, kTileAlphaRing = 3;
 constexpr int kTileFwdWait = kTileRowAhead - 2;   // row k+2 complete at the end of frame k
 constexpr int kTileBwdWait = kTileAlphaAhead - 1; // alpha t-2 / row t-3 at the end of frame t
 static_assert(kTileBwdWait <= kTileRowAhead - 2, "row pipeline must be at least as deep");
+
+// Numerator-sized CTAs (<= 128 threads): registers capped so that several
+// utterances share an SM (the numerator pass runs on the SMs the denominator
+// pass leaves free).
+#ifndef LFMMI_NUM_MIN_BLOCKS
+#define LFMMI_NUM_MIN_BLOCKS 6
+#endif
+constexpr int kNumMinBlocks = LFMMI_NUM_MIN_BLOCKS;
 
 struct TileLayout {  // byte offsets of one utterance's slice of shared memory
   size_t wp, xs, tinfo, ttrips, tbase, wlist, wtab, pdfptr, xterm, rbuf, aring, ebuf, stage,
@@ -104,7 +113,7 @@ __device__ __forceinline__ void tsync() {
 // work — instead of between two extra barriers; tiles then follow the host's
 // LPT warp lists, which give the flushing warps fewer arcs.
 template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI, bool XDB = false>
-__global__ void __launch_bounds__(GROUP *IPC, 1)
+__global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks : 1)
     fb_tile_kernel(const FBArgs<Real> a, int Fmax, int ntiles_max, int X_pad) {
   static_assert(!XDB || (GROUP == 32 * kTableNW && IPC == 1 && SMEM_GRAPH),
                 "XDB uses the 16-warp LPT lists");
@@ -332,6 +341,14 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
   gsync();
   read_warps();
 
+  // debug section timestamps (LFMMI_PROFILE_TILE): fwd start/end, bwd start/end
+  auto stamp = [&](int j) {
+    if (a.prof != nullptr && tid == 0) {
+      a.prof[size_t(b) * 8 + j] = clock64();
+      a.prof[size_t(b) * 8 + 6] = T;
+    }
+  };
+  stamp(0);
   // ---- forward: one barrier per frame ------------------------------------------------
   Real inv2 = Real(1), leakc = Real(0);
   int fail_at = -1;
@@ -437,6 +454,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     row_max_part(k + 2);
     gsync();
   }
+  stamp(1);
   if (fail_at < 0) {
     const Real t0 = lane_sum<NW>(part + (T & 1) * 32, lane);
     Real t2 = t0;
@@ -553,6 +571,7 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
 
   const bool flusher = cwarp * 32 < D * spl;
   Real sc_cur = scales[T - 1];
+  stamp(2);
   for (int t = T; t >= 1; --t) {
     const int ct = t & 1, cp = ct ^ 1;
     Real ld = Real(0);
@@ -621,7 +640,10 @@ __global__ void __launch_bounds__(GROUP *IPC, 1)
     }
   }
   if (XDB && flusher) flush_post(0, xterm + X_pad);  // frame 0: written at t = 1
+  stamp(3);
 }
+
+constexpr int kDenGroupC = 512;
 
 template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH, bool CUSTOM_PI, bool XDB = false>
 static int launch_tile_impl2(const FBArgs<Real> &a, const lfmmi_graphs *g, size_t per_item,
@@ -637,9 +659,35 @@ static int launch_tile_impl2(const FBArgs<Real> &a, const lfmmi_graphs *g, size_
   }
   const int grid = (a.B + IPC - 1) / IPC;
   const int Fmax = std::max(g->max_tf_slots, g->max_tb_slots);
-  kern<<<grid, GROUP * IPC, per_item * IPC, st>>>(a, Fmax, g->max_tiles,
+  if (GROUP != kDenGroupC || !std::getenv("LFMMI_PROFILE_TILE")) {
+    kern<<<grid, GROUP * IPC, per_item * IPC, st>>>(a, Fmax, g->max_tiles,
+                                                    pad4(std::max(4, g->max_xpad)));
+    return check_cuda(cudaGetLastError(), "fb_tile_kernel launch");
+  }
+  // Debug: forward / backward cycles per frame (mean over utterances) on stderr.
+  FBArgs<Real> ap = a;
+  long long *d = nullptr;
+  cudaMalloc(&d, size_t(a.B) * 8 * sizeof(long long));
+  cudaMemsetAsync(d, 0, size_t(a.B) * 8 * sizeof(long long), st);
+  ap.prof = d;
+  kern<<<grid, GROUP * IPC, per_item * IPC, st>>>(ap, Fmax, g->max_tiles,
                                                   pad4(std::max(4, g->max_xpad)));
-  return check_cuda(cudaGetLastError(), "fb_tile_kernel launch");
+  const int rc = check_cuda(cudaGetLastError(), "fb_tile_kernel launch");
+  std::vector<long long> hp(size_t(a.B) * 8);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(hp.data(), d, hp.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  double fw = 0, bw = 0, fr = 0;
+  for (int i = 0; i < a.B; ++i) {
+    const long long *p = &hp[size_t(i) * 8];
+    if (!p[3]) continue;
+    fw += double(p[1] - p[0]);
+    bw += double(p[3] - p[2]);
+    fr += double(p[6]);
+  }
+  std::fprintf(stderr, "[lfmmi tile prof] forward %.0f  backward %.0f cycles/frame\n", fw / fr,
+               bw / fr);
+  return rc;
 }
 
 template <typename Real, int GROUP, int IPC, bool SMEM_GRAPH>
