@@ -96,7 +96,8 @@ __device__ __forceinline__ void cluster_barrier() {
 }  // namespace
 
 __global__ void __launch_bounds__(kNT, 1)
-    fb_split_kernel(const FBArgs<float> a, int Fmax, int ntiles_max, int X_pad, int nclusters) {
+    fb_split_kernel(const FBArgs<float> a, int Fmax, int ntiles_max, int X_pad, int nclusters,
+                    int hnum) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ctid = kNT - 1 - tid, cwarp = ctid >> 5;  // chores on the last warps
@@ -114,7 +115,6 @@ __global__ void __launch_bounds__(kNT, 1)
   float *ebuf = reinterpret_cast<float *>(smem + lay.ebuf);
   float *stage = reinterpret_cast<float *>(smem + lay.stage);
   float *part = reinterpret_cast<float *>(smem + lay.part);
-  float *partz = reinterpret_cast<float *>(smem + lay.partz);
   float *mpart = reinterpret_cast<float *>(smem + lay.mpart);
   int *items = reinterpret_cast<int *>(smem + lay.items);
   const uint32_t wp32 = smem_u32(smem + lay.wp), xs32 = smem_u32(smem + lay.xs);
@@ -225,7 +225,10 @@ __global__ void __launch_bounds__(kNT, 1)
     const int S = desc[kS], init = desc[kInit];
     const float *fin = a.g.fin32 + desc[kStateOff];
     const float upi = float(1.0 / double(S));
-    const int h = T / 2;  // forward CTA: posteriors of frames >= h; backward CTA: < h
+    // forward CTA: posteriors of frames >= h; backward CTA: < h.  The forward
+    // posterior frame costs ~7% more than the backward one (measured, WSJ-mono),
+    // so the forward CTA takes slightly fewer: h = T * hnum / 64, <= T - 1.
+    const int h = min(T - 1, (T * hnum + 32) >> 6);
     const bool other_failed = a.other_fail != nullptr && a.other_fail[b] >= 0;
 
     if (a.prof != nullptr && tid == 0)
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(kNT, 1)
       v[s] = x;
       if (rep2) v[rstride + s] = x;
     };
-    auto flush_post = [&](int t, const float *xsrc, float invz) {
+    auto flush_post = [&](int t, const float *xsrc) {
       float *prow = post_b + size_t(t) * D;
       const int sub = ctid & (spl - 1);
       for (int base_i = 0; base_i < D * spl; base_i += kNT) {
@@ -310,7 +313,19 @@ __global__ void __launch_bounds__(kNT, 1)
           for (int q = lo + sub; q < hi; q += spl) g += sum_groups4(xsrc + 4 * q, 1);
         }
         for (int o = 1; o < spl; o <<= 1) g += __shfl_xor_sync(kFull, g, o);
-        if (d < D && sub == 0) prow[d] = negate ? -(g * invz) : g * invz;
+        if (d < D && sub == 0) prow[d] = negate ? -g : g;
+      }
+    };
+    // Posterior rows [f0, f1) of this CTA: divide by Z_f = |sum of the row| (the
+    // sum of all arc terms of frame f), one warp per row, after the last flush.
+    auto normalize_rows = [&](int f0, int f1) {
+      for (int f = f0 + warp; f < f1; f += kNW) {
+        float *prow = post_b + size_t(f) * D;
+        float z = 0.f;
+        for (int d = lane; d < D; d += 32) z += prow[d];
+        z = warp_sum(z);
+        const float iz = rcp_rn(fabsf(z));
+        for (int d = lane; d < D; d += 32) prow[d] *= iz;
       }
     };
     bool mid_done = false;
@@ -378,9 +393,7 @@ __global__ void __launch_bounds__(kNT, 1)
             a4[q] = v;
           }
         }
-        if (POST && k - 1 >= h && flusher)
-          flush_post(k - 1, xterm + ((k - 1) & 1) * X_pad,
-                     rcp_rn(lane_sum<kNW>(partz + ((k - 1) & 1) * 32, lane)));
+        if (POST && k - 1 >= h && flusher) flush_post(k - 1, xterm + ((k - 1) & 1) * X_pad);
         if (k + 1 < T) compute_e(k + 1, true);
         issue_row(k + kRowAhead);
         if (POST) issue_trellis(k + kRingAhead);
@@ -389,7 +402,7 @@ __global__ void __launch_bounds__(kNT, 1)
           const uint32_t e32 = smem_u32(ebuf + cur * EB), r32 = smem_u32(rbuf + cur * RB);
           float *rn = rbuf + nxt * RB;
           const bool last = (k + 1 == T);
-          float psum = 0.f, zp = 0.f;
+          float psum = 0.f;
           for (int rr = wlo; rr < whi; ++rr) {
             const int tile = wl[rr];
             const unsigned info = tinfo[tile * 32 + lane];
@@ -404,7 +417,6 @@ __global__ void __launch_bounds__(kNT, 1)
                                                 xs32 + uint32_t(base) * 2u, trips, e32, r32,
                                                 smem_u32(xterm + (k & 1) * X_pad), lu, cb);
               raw = inv2 * A;
-              zp = fmaf(cb, A, zp);
             } else {
               float A = 0.f, Bs = 0.f;
               if (leakc != 0.f)
@@ -421,10 +433,6 @@ __global__ void __launch_bounds__(kNT, 1)
           }
           psum = warp_sum(psum);
           if (lane == 0) part[nxt * 32 + warp] = psum;
-          if constexpr (POST) {
-            zp = warp_sum(zp);
-            if (lane == 0) partz[(k & 1) * 32 + warp] = zp;
-          }
         }
         // plain frames: log-likelihood rows only, two frames of slack; posterior
         // frames: the trellis row issued last frame must land too
@@ -466,9 +474,11 @@ __global__ void __launch_bounds__(kNT, 1)
           fail_at = T - 1;
         else if (tid == 0)
           scales[T - 1] = t2;
-        if (!other_failed && flusher)  // frame T-1 (h <= T-1 always)
-          flush_post(T - 1, xterm + ((T - 1) & 1) * X_pad,
-                     rcp_rn(lane_sum<kNW>(partz + ((T - 1) & 1) * 32, lane)));
+        if (!other_failed) {  // frame T-1 (h <= T-1 always), then rows h..T-1
+          if (flusher) flush_post(T - 1, xterm + ((T - 1) & 1) * X_pad);
+          __syncthreads();
+          normalize_rows(h, T);
+        }
       }
       if (!mid_done) cluster_barrier();  // failed before the midpoint
       if (fail_at >= 0) {
@@ -554,8 +564,7 @@ __global__ void __launch_bounds__(kNT, 1)
             }
           }
           if (POST && t < h && flusher)  // frame t (posterior, previous iteration)
-            flush_post(t, xterm + (t & 1) * X_pad,
-                       rcp_rn(lane_sum<kNW>(partz + (t & 1) * 32, lane)));
+            flush_post(t, xterm + (t & 1) * X_pad);
           if (t - 2 >= 0) compute_e(t - 2, false);
           issue_row(t - 1 - kRowAhead);
           if (POST) issue_trellis(f - kRingAhead);
@@ -563,7 +572,7 @@ __global__ void __launch_bounds__(kNT, 1)
           {
             const uint32_t e32 = smem_u32(ebuf + cpar * EB), b32 = smem_u32(rbuf + ct * RB);
             float *bn = rbuf + cpar * RB;
-            float dq = 0.f, zp = 0.f;
+            float dq = 0.f;
             for (int rr = wlo; rr < whi; ++rr) {
               const int tile = wl[rr];
               const unsigned info = tinfo[tile * 32 + lane];
@@ -576,7 +585,6 @@ __global__ void __launch_bounds__(kNT, 1)
                 const float as = s != 0xFFFF ? al[s] : 0.f;
                 A = bwd_tile_f32(wp32 + uint32_t(base) * 8u, xs32 + uint32_t(base) * 2u, trips,
                                  e32, b32, smem_u32(xterm + (f & 1) * X_pad), ld, as);
-                zp = fmaf(as, A, zp);
               } else {
                 A = bwd_plain_tile_f32(wp32 + uint32_t(base) * 8u, trips, e32, b32, ld);
               }
@@ -588,10 +596,6 @@ __global__ void __launch_bounds__(kNT, 1)
             }
             dq = warp_sum(dq);
             if (lane == 0) part[cpar * 32 + warp] = dq;
-            if constexpr (POST) {
-              zp = warp_sum(zp);
-              if (lane == 0) partz[(f & 1) * 32 + warp] = zp;
-            }
           }
           if constexpr (POST)
             cp_async_wait<kWait>();
@@ -613,8 +617,11 @@ __global__ void __launch_bounds__(kNT, 1)
           stamp(3);
           for (int t = h; t >= 1; --t) bframe(t, std::true_type{});
         }
-        if (h >= 1 && flusher)
-          flush_post(0, xterm, rcp_rn(lane_sum<kNW>(partz, lane)));
+        if (h >= 1) {
+          if (flusher) flush_post(0, xterm);
+          __syncthreads();
+          normalize_rows(0, h);
+        }
       }
       if (!mid_done) cluster_barrier();
       stamp(4);
@@ -673,6 +680,8 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
     if (rc) return rc;
     configured = true;
   }
+  const char *h_env = std::getenv("LFMMI_SPLIT_H64");  // midpoint in 64ths of T (A/B)
+  const int hnum = h_env ? std::max(0, std::min(64, std::atoi(h_env))) : 33;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * nc);
   cfg.blockDim = dim3(kNT);
@@ -693,7 +702,7 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   }
   note_den_kernel("fb_split_kernel (2-CTA cluster: forward | backward)");
   if (!std::getenv("LFMMI_PROFILE_SPLIT"))
-    return check_cuda(cudaLaunchKernelEx(&cfg, kern, b, Fmax, g->max_tiles, X_pad, nc),
+    return check_cuda(cudaLaunchKernelEx(&cfg, kern, b, Fmax, g->max_tiles, X_pad, nc, hnum),
                       "fb_split_kernel launch");
   // Debug: per-item section timestamps of both CTAs, summarised on stderr.
   const size_t n = size_t(2 * nc) * kMaxItems * 8;
@@ -702,7 +711,7 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   if (rc) return rc;
   cudaMemsetAsync(d, 0, n * sizeof(long long), st);
   b.prof = d;
-  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, b, Fmax, g->max_tiles, X_pad, nc),
+  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, b, Fmax, g->max_tiles, X_pad, nc, hnum),
                   "fb_split_kernel launch");
   std::vector<long long> hp(n);
   cudaStreamSynchronize(st);

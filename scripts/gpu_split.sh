@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 LFMMI_DEBUG=1 timeout 300 python scripts/time_passes.py wsj_mono > gpurun_out/split_passes.log 2>&1
 echo "passes rc=$?"
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu > gpurun_out/split_pytest.log 2>&1
+timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/split_pytest.log 2>&1
 echo "pytest rc=$?"
 tail -5 gpurun_out/split_pytest.log
 grep -v Warning gpurun_out/split_passes.log | grep -v "^  t(" | tail -12
