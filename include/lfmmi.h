@@ -57,9 +57,9 @@ const char *lfmmi_version(void);
 int32_t lfmmi_last_launch_count(void);
 
 /*
- * Name of the kernel that ran the last denominator-sized (one CTA or cluster
- * per utterance) forward-backward on this thread, e.g. "fb_split_kernel".
- * Diagnostic (benchmarks label their roofline line with it).
+ * Name of the kernel that ran the last forward-backward pass launched on this
+ * thread, e.g. "fb_split_kernel ..." for a WSJ-sized denominator.  Diagnostic
+ * (benchmarks label their roofline line with it).
  */
 const char *lfmmi_last_den_kernel(void);
 
