@@ -201,6 +201,9 @@ __global__ void __launch_bounds__(kNT, 1)
     }
     const int *pp = a.g.pdf_arc_ptr + desc[kPdfPtrOff2];
     for (int d = tid; d <= D; d += kNT) pdfptr[d] = pp[d];
+    // padding slots of the per-pdf groups are never written: zero them once per
+    // pack (the buffers also held the scheduling scratch)
+    for (int i = tid; i < 2 * X_pad; i += kNT) xterm[i] = 0.f;
     cp_async_commit();
     cp_async_wait<0>();
     bound_row = row;
@@ -239,9 +242,6 @@ __global__ void __launch_bounds__(kNT, 1)
     __syncthreads();  // previous item's readers of the scratch are done
     if (lane == 0) lscr[warp] = off;
     if (row != bound_row) bind(row);
-    // xterm: padding slots of the per-pdf groups are never written (zero once per item,
-    // it also held the scheduling scratch)
-    for (int i = tid; i < 2 * X_pad; i += kNT) xterm[i] = 0.f;
     __syncthreads();
     long long item_off = 0;
     for (int w = 0; w < kNW; ++w) item_off += lscr[w];
