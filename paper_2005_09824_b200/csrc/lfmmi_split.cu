@@ -223,6 +223,18 @@ __global__ void __launch_bounds__(kNT, 1)
   for (int it = 0; it < nitems; ++it) {
     const int b = items[4 + it];
     const int T = a.lengths[b];
+    if (T <= 0) {  // zero-length item (host APIs reject it): failed, no frames touched
+      if (fwd) {
+        if (!a.packed)
+          for (size_t i = tid; i < size_t(a.T_max) * D; i += kNT)
+            a.post[size_t(b) * a.T_max * D + i] = 0.f;
+        if (tid == 0) {
+          a.logp[b] = NAN;
+          a.fail[b] = 0;
+        }
+      }
+      continue;  // no barriers: both CTAs skip it
+    }
     const int row = int(a.row_map[b]);
     const int *desc = a.g.desc + row * kDescInts;
     const int S = desc[kS], init = desc[kInit];

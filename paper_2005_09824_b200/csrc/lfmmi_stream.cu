@@ -108,6 +108,18 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   }
 
   const int T = a.lengths[b];
+  if (T <= 0) {  // zero-length item (host APIs reject it): failed, no frames touched
+    if (rank == 0) {
+      if (!a.packed)
+        for (size_t i = threadIdx.x; i < size_t(a.T_max) * a.D; i += NT)
+          a.post[size_t(b) * a.T_max * a.D + i] = 0.f;
+      if (threadIdx.x == 0) {
+        a.logp[b] = NAN;
+        a.fail[b] = 0;
+      }
+    }
+    return;  // both CTAs of a cluster see the same T
+  }
   const int D = a.D, D_pad = a.D_pad;
   const int row = int(a.row_map[b]);
   const int *desc = a.g.desc + row * kDescInts;

@@ -154,6 +154,16 @@ __global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks 
   (void)xs32;
 
   const int T = a.lengths[b];
+  if (T <= 0) {  // zero-length item (host APIs reject it): failed, no frames touched
+    if (a.mode != kPostAdd && a.mode != kPostSubtract && !a.packed)
+      for (size_t i = tid; i < size_t(a.T_max) * a.D; i += GROUP)
+        a.post[size_t(b) * a.T_max * a.D + i] = Real(0);
+    if (tid == 0) {
+      a.logp[b] = NAN;
+      a.fail[b] = 0;
+    }
+    return;
+  }
   const int D = a.D;
   const int S_pad = a.S_pad, D_pad = a.D_pad;
   const int row = int(a.row_map[b]);

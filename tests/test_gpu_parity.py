@@ -435,6 +435,34 @@ def test_packed_ragged_batch_any_order(cuda, config, batch_size, kernel, monkeyp
         assert _rel(nl[k], ref.per_utt[b][0]) <= 1e-5
 
 
+@pytest.mark.parametrize("kernel", ["auto", "tile", "split1"])
+def test_zero_length_item_fails_alone(cuda, kernel, monkeypatch):
+    """The device APIs take lengths as a device tensor and do not read them back:
+    a zero-length utterance is reported failed (NaN log-prob, failure frame 0)
+    without touching memory, and the rest of the batch is unaffected."""
+    import torch
+
+    _kernel_env(kernel, monkeypatch)
+    w = synth.make_workload("wsj_mono", seed=12, batch_size=4)
+    batch, nums, den = w.build(P)
+    ref = O.chain_loss(batch, nums, den, leak=1e-5)
+    seqs = [batch.values[b, :batch.lengths[b]] for b in range(4)]
+    dev = torch.device("cuda", 0)
+    x = torch.tensor(np.concatenate(seqs), dtype=torch.float32, device=dev)
+    lens = torch.tensor([len(seqs[0]), 0, *[len(q) for q in seqs[1:]]], dtype=torch.int32,
+                        device=dev)
+    num_list = [nums.graph(0), nums.graph(0), nums.graph(1), nums.graph(2), nums.graph(3)]
+    g, nl, dl, nf, df, tot = P.chain_loss_packed(x, lens, num_list, den.graph(0))
+    tot = tot.cpu().numpy()
+    assert int(round(tot[2])) == 1 and int(round(tot[1])) == int(batch.lengths.sum())
+    assert _rel(float(tot[0]), ref.objective) <= FP32_OBJ_REL
+    assert math.isnan(float(dl[1].cpu())) and int(df[1].cpu()) == 0
+    g = g.double().cpu().numpy()
+    offs = np.concatenate([[0], np.cumsum([len(q) for q in seqs])])
+    for b in range(4):
+        assert np.abs(g[offs[b]:offs[b + 1]] - ref.grad[b, :batch.lengths[b]]).max() <= FP32_GRAD_ABS
+
+
 def test_chain_function_packed_input(cuda):
     import torch
 
