@@ -26,6 +26,8 @@
 #include <random>
 #include <cstdlib>
 #include <numeric>
+#include <functional>
+#include <cstdio>
 
 namespace lfmmi {
 
@@ -417,35 +419,99 @@ void assign_xslots(const TileSchedule &tb, const int *pdf_of_arc, int num_pdfs, 
     for (int pos = pdf_ptr[p + 1] - 1; pos >= pdf_ptr[p]; --pos)
       freel[size_t(p) * 32 + (pos & 31)].push_back(pos);
   xslot_of_slot.assign(tb.arc.size(), dummy);
+  static const bool greedy_only = std::getenv("LFMMI_XSLOT_GREEDY") != nullptr;
+  long waves = 0, rows = 0;
   for (size_t w = 0; w < tb.trips.size(); ++w) {
     for (int j = 0; j < tb.trips[w]; ++j) {
-      bool used[32] = {false};
       const size_t row = size_t(tb.base[w]) + size_t(32) * j;
-      for (int l = 0; l < 32; ++l)
-        if (tb.arc[row + l] < 0) used[dummy & 31] = true;
+      // Each lane's store goes to a bank where its pdf still has a free
+      // position; a row costs one wavefront per store in its busiest bank.
+      // Maximum bipartite matching lanes -> banks (augmenting paths, lanes with
+      // the fewest candidate banks first, banks with the most free positions
+      // first), then the unmatched lanes go to their roomiest bank.
+      int bank_of[32], lane_of_bank[32], order[32], nopt[32];
+      std::fill(bank_of, bank_of + 32, -1);
+      std::fill(lane_of_bank, lane_of_bank + 32, -1);
+      bool used_dummy = false;
+      int nl = 0;
       for (int l = 0; l < 32; ++l) {
         const int a = tb.arc[row + l];
-        if (a < 0) continue;
-        const int p = pdf_of_arc[a];
-        int bank = -1, bank_any = -1;
-        size_t most = 0;
-        for (int b = 0; b < 32; ++b) {
-          const size_t nfree = freel[size_t(p) * 32 + b].size();
-          if (!nfree) continue;
-          if (bank_any < 0) bank_any = b;
-          if (!used[b] && nfree > most) {
-            most = nfree;
-            bank = b;
-          }
+        if (a < 0) {
+          used_dummy = true;
+          continue;
         }
-        if (bank < 0) bank = bank_any;
-        auto &fl = freel[size_t(p) * 32 + bank];
+        const int p = pdf_of_arc[a];
+        nopt[l] = 0;
+        for (int b = 0; b < 32; ++b) nopt[l] += !freel[size_t(p) * 32 + b].empty();
+        order[nl++] = l;
+      }
+      if (used_dummy) lane_of_bank[dummy & 31] = 32;  // padding lanes' store (dummy slot)
+      std::stable_sort(order, order + nl, [&](int x, int y) { return nopt[x] < nopt[y]; });
+      auto pdf_l = [&](int l) { return pdf_of_arc[tb.arc[row + l]]; };
+      auto cands = [&](int l, int *bs) {  // candidate banks, most free positions first
+        const int p = pdf_l(l);
+        int n = 0;
+        for (int b = 0; b < 32; ++b)
+          if (!freel[size_t(p) * 32 + b].empty()) bs[n++] = b;
+        std::stable_sort(bs, bs + n, [&](int x, int y) {
+          return freel[size_t(p) * 32 + x].size() > freel[size_t(p) * 32 + y].size();
+        });
+        return n;
+      };
+      if (!greedy_only) {
+        for (int k = 0; k < nl; ++k) {
+          const int l0 = order[k];
+          bool seen[32] = {false};
+          // DFS augmenting path from l0
+          std::function<bool(int)> aug = [&](int l) -> bool {
+            int bs[32];
+            const int n = cands(l, bs);
+            for (int q = 0; q < n; ++q) {
+              const int b = bs[q];
+              if (seen[b]) continue;
+              seen[b] = true;
+              const int o = lane_of_bank[b];
+              if (o == 32) continue;  // reserved for the padding lanes
+              if (o < 0 || aug(o)) {
+                lane_of_bank[b] = l;
+                bank_of[l] = b;
+                return true;
+              }
+            }
+            return false;
+          };
+          aug(l0);
+        }
+      }
+      int mult[32] = {0};
+      if (used_dummy) mult[dummy & 31] = 1;
+      for (int k = 0; k < nl; ++k) {
+        const int l = order[k];
+        const int p = pdf_l(l);
+        int b = bank_of[l];
+        if (b < 0 || freel[size_t(p) * 32 + b].empty()) {  // unmatched: least-loaded bank
+          int best = -1;
+          for (int c = 0; c < 32; ++c) {
+            if (freel[size_t(p) * 32 + c].empty()) continue;
+            if (best < 0 || mult[c] < mult[best] ||
+                (mult[c] == mult[best] &&
+                 freel[size_t(p) * 32 + c].size() > freel[size_t(p) * 32 + best].size()))
+              best = c;
+          }
+          b = best;
+        }
+        auto &fl = freel[size_t(p) * 32 + b];
         xslot_of_slot[row + l] = fl.back();
         fl.pop_back();
-        used[bank] = true;
+        ++mult[b];
       }
+      waves += *std::max_element(mult, mult + 32);
+      ++rows;
     }
   }
+  if (std::getenv("LFMMI_DEBUG_XSLOT"))
+    std::fprintf(stderr, "[lfmmi] xslot stores: %ld rows, %.3f wavefronts/row (%s)\n", rows,
+                 rows ? double(waves) / double(rows) : 0.0, greedy_only ? "greedy" : "matching");
 }
 
 void warp_lists(const std::vector<int> &trips, const std::vector<int> &bias,

@@ -52,11 +52,12 @@ constexpr int kTileFwdWait = kTileRowAhead - 2;   // row k+2 complete at the end
 constexpr int kTileBwdWait = kTileAlphaAhead - 1; // alpha t-2 / row t-3 at the end of frame t
 static_assert(kTileBwdWait <= kTileRowAhead - 2, "row pipeline must be at least as deep");
 
-// Numerator-sized CTAs (<= 128 threads): registers capped so that several
-// utterances share an SM (the numerator pass runs on the SMs the denominator
-// pass leaves free).
+// Numerator-sized CTAs (<= 128 threads): registers capped (<= 72) so that 7
+// utterances share an SM — the numerator pass runs on the 20 SMs the split
+// denominator leaves free, and 128 numerators must be resident at once (at 75
+// registers only 6 fit: the pass grew from 1.04 to ~1.13 ms).
 #ifndef LFMMI_NUM_MIN_BLOCKS
-#define LFMMI_NUM_MIN_BLOCKS 6
+#define LFMMI_NUM_MIN_BLOCKS 7
 #endif
 constexpr int kNumMinBlocks = LFMMI_NUM_MIN_BLOCKS;
 

@@ -35,5 +35,9 @@ int main() {
         rows++; wr += mr; we += me;
       }
     printf("optimize=%d rows=%ld r-gather wavefronts=%ld (%.2f/row) e-gather=%ld (%.2f/row)\n", opt, rows, wr, double(wr)/rows, we, double(we)/rows);
+    if (opt) {  // posterior-slot stores (LFMMI_DEBUG_XSLOT prints wavefronts/row)
+      std::vector<int> pp, xs; int xpad = 0;
+      assign_xslots(ts, pd.data(), D, I, 4, pp, xs, xpad);
+    }
   }
 }
