@@ -283,7 +283,7 @@ def run_ours(args):
     # ---- dominant kernel timed alone (no collective), same inputs -----------
     # Fused path (LFMMI_FUSED=1): the single chain launch.  Two-pass path
     # (default): the denominator pass, the step's critical path (the numerator
-    # pass runs concurrently on an auxiliary stream; combine + totals ~15 us).
+    # pass runs concurrently on an auxiliary stream; combine + totals ~10 us).
     launches_per_step = int(ext.last_launch_count())
     fused = launches_per_step == 1
 

@@ -52,7 +52,8 @@ const char *lfmmi_version(void);
 
 /*
  * Number of kernels the last successful lfmmi_chain_loss call on this thread
- * launched (1 = fused single-launch path, 4 = two-pass path).  Diagnostic.
+ * launched (1 = fused single-launch path, 3 = two-pass path: denominator,
+ * numerators, gradient combine + batch totals).  Diagnostic.
  */
 int32_t lfmmi_last_launch_count(void);
 

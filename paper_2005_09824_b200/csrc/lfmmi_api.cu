@@ -178,9 +178,11 @@ __global__ void post_parity_kernel(DevGraphs g, const int64_t *row_map, int B, i
   }
 }
 
-// Batch totals for chain_loss (loss.py:61-72), fixed-order reduction.
-__global__ void totals_kernel(int B, const int *lengths, const double *num_lp, const double *den_lp,
-                              const int *num_fail, const int *den_fail, double *totals) {
+// Batch totals for chain_loss (loss.py:61-72), fixed-order reduction by one
+// 256-thread block (block (0, 0) of combine_kernel).
+__device__ void batch_totals(int B, const int *lengths, const double *num_lp,
+                             const double *den_lp, const int *num_fail, const int *den_fail,
+                             double *totals) {
   __shared__ double so[256], sf[256], sn[256];
   double o = 0.0, f = 0.0, n = 0.0;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
@@ -398,7 +400,10 @@ extern "C" size_t lfmmi_chain_loss_workspace_size(const lfmmi_graphs *numerators
 template <typename Real>
 __global__ void combine_kernel(bool packed, int B, int T_max, int D, const int *lengths,
                                const int *num_fail, const int *den_fail,
-                               const Real *__restrict__ gnum, Real *__restrict__ grad) {
+                               const Real *__restrict__ gnum, Real *__restrict__ grad,
+                               const double *num_lp, const double *den_lp, double *totals) {
+  if (totals != nullptr && blockIdx.x == 0 && blockIdx.y == 0)  // one launch for both
+    batch_totals(B, lengths, num_lp, den_lp, num_fail, den_fail, totals);
   const size_t row_elems = size_t(T_max) * D;
   for (int b = blockIdx.y; b < B; b += gridDim.y) {
     const size_t n = size_t(lengths[b]) * D;
@@ -566,21 +571,18 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
       combine_kernel<double><<<grid, 256, 0, st>>>(packed, batch, max_frames, num_pdfs, lengths, num_fail,
                                                    den_fail,
                                                    reinterpret_cast<const double *>(ws + gam_off),
-                                                   static_cast<double *>(grad));
+                                                   static_cast<double *>(grad), num_log_probs,
+                                                   den_log_probs, totals);
     else
       combine_kernel<float><<<grid, 256, 0, st>>>(packed, batch, max_frames, num_pdfs, lengths, num_fail,
                                                   den_fail,
                                                   reinterpret_cast<const float *>(ws + gam_off),
-                                                  static_cast<float *>(grad));
+                                                  static_cast<float *>(grad), num_log_probs,
+                                                  den_log_probs, totals);
     rc = check_cuda(cudaGetLastError(), "combine_kernel launch");
     if (rc) return rc;
   }
-  if (totals) {
-    totals_kernel<<<1, 256, 0, st>>>(batch, lengths, num_log_probs, den_log_probs, num_fail,
-                                     den_fail, totals);
-    rc = check_cuda(cudaGetLastError(), "totals_kernel launch");
-  }
-  g_launches = rc == LFMMI_OK ? (totals ? 4 : 3) : 0;
+  g_launches = rc == LFMMI_OK ? 3 : 0;  // den, num, combine (+ totals)
   return rc;
 }
 
