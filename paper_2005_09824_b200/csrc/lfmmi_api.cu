@@ -415,6 +415,28 @@ __global__ void combine_kernel(bool packed, int B, int T_max, int D, const int *
     }
     Real *g = grad + base;
     const Real *q = gnum + base;
+    if constexpr (sizeof(Real) == 4) {
+      // every item's rows start 16-byte aligned when D % 4 == 0 (and the bases are)
+      if ((D & 3) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(q)) & 15) == 0) {
+        float4 *g4 = reinterpret_cast<float4 *>(g);
+        const float4 *q4 = reinterpret_cast<const float4 *>(q);
+        for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (n >> 2);
+             i += size_t(gridDim.x) * blockDim.x) {
+          float4 v = g4[i];
+          const float4 u = q4[i];
+          if (ok) {
+            v.x += u.x;
+            v.y += u.y;
+            v.z += u.z;
+            v.w += u.w;
+          } else {
+            v = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          g4[i] = v;
+        }
+        continue;
+      }
+    }
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += size_t(gridDim.x) * blockDim.x)
       g[i] = ok ? g[i] + q[i] : Real(0);
@@ -565,7 +587,7 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
   rc = check_cuda(cudaStreamWaitEvent(st, ax.join, 0), "cudaStreamWaitEvent(join)");
   if (rc) return rc;
   {
-    const dim3 grid(std::max(1, std::min(32, (max_frames * num_pdfs + 1023) / 1024)),
+    const dim3 grid(std::max(1, std::min(32, (max_frames * num_pdfs + 4095) / 4096)),
                     std::min(batch, 4096));
     if (precision == LFMMI_F64)
       combine_kernel<double><<<grid, 256, 0, st>>>(packed, batch, max_frames, num_pdfs, lengths, num_fail,
