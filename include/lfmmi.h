@@ -47,6 +47,20 @@ typedef struct lfmmi_graphs lfmmi_graphs;
 /* Message describing the last nonzero status returned on this thread. */
 const char *lfmmi_last_error(void);
 
+/*
+ * Process-wide dispatch / debug options, one struct parsed once from the
+ * LFMMI_OPTIONS environment variable ("name=value,...") and changeable here.
+ * Names: tile, stream, linear (0/1: kernel families the dispatcher may use),
+ * split (-1 auto / 0 off / 1 force), split_clusters (0 auto), split_h64,
+ * stream_mode ("auto", "1024x1", "1024x2", "512x2"), num_group, tile_xdb,
+ * serial, sched_iters (-1 auto), debug, profile ("", "split", "tile").
+ * Unknown names return LFMMI_ERR_INVALID.  Not thread-safe against
+ * concurrent launches: set them before use.
+ */
+int lfmmi_set_option(const char *name, const char *value);
+int lfmmi_get_option(const char *name, char *buf, size_t len);
+int lfmmi_reset_options(void);
+
 /* Library version string. */
 const char *lfmmi_version(void);
 
@@ -80,6 +94,25 @@ int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t max_arcs, 
                         const double *fw_prob, const uint32_t *bw_from, const uint32_t *bw_to,
                         const uint32_t *bw_pdf, const double *bw_prob, const double *final_probs,
                         const uint32_t *initial_states, lfmmi_graphs **out);
+
+/*
+ * Graph batch of LINEAR CHAINS from caller-owned DEVICE arrays: no copy, no
+ * allocation, no synchronisation — a training step assembles it from cached
+ * per-utterance records with one async H2D copy.  A linear chain has only
+ * self-loops s -> s and entry arcs s-1 -> s, at most one of each per state
+ * (the reference's numerators: toy_builder.py:218-265 build_numerator).
+ *   items   (num_rows x 4) int32: state offset into `states`, S, initial state, 0
+ *   states  (sum S x 4)  u32 per state: fp32 bits of the self-loop prob (0 if
+ *           none), fp32 bits of the entry-arc prob (0 if none), self pdf |
+ *           entry pdf << 16, fp32 bits of the final prob
+ * max_states <= 512, num_pdfs <= 65536.  The arrays must outlive the handle
+ * and every launch that uses it; lfmmi_graphs_destroy frees only the handle.
+ * Such a handle is usable by the fp32 paths with the uniform leak only.
+ * (lfmmi_graphs_create builds the same records itself when every row of a
+ * host batch is a linear chain.)
+ */
+int lfmmi_graphs_create_linear(int32_t num_rows, int32_t max_states, int32_t num_pdfs,
+                               const int32_t *items, const uint32_t *states, lfmmi_graphs **out);
 
 int lfmmi_graphs_destroy(lfmmi_graphs *graphs);
 

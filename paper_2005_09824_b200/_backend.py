@@ -3,6 +3,7 @@ extension or a GPU is missing, every compute entry point raises."""
 
 from __future__ import annotations
 
+import contextlib
 import importlib.machinery
 import importlib.util
 import os
@@ -45,3 +46,18 @@ def require_cuda():
 
 def core_library_path() -> str:
     return _build.CORE_SO
+
+
+@contextlib.contextmanager
+def options(**kw):
+    """Temporarily set library options (``lfmmi_set_option``; include/lfmmi.h):
+    ``with options(split=0, stream_mode="1024x1"): ...``."""
+    e = ext()
+    old = {k: e.get_option(k) for k in kw}
+    try:
+        for k, v in kw.items():
+            e.set_option(k, str(v))
+        yield
+    finally:
+        for k, v in old.items():
+            e.set_option(k, v)

@@ -26,9 +26,9 @@ TORCH_SO = os.path.join(LIB_DIR, "_lfmmi_torch" + (sysconfig.get_config_var("EXT
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CORE_SOURCES = ["lfmmi_api.cu", "lfmmi_group.cu", "lfmmi_tile.cu", "lfmmi_chain.cu", "lfmmi_stream.cu", "lfmmi_split.cu",
+CORE_SOURCES = ["lfmmi_api.cu", "lfmmi_group.cu", "lfmmi_tile.cu", "lfmmi_linear.cu", "lfmmi_stream.cu", "lfmmi_split.cu",
                 "lfmmi_graph.cpp",
-                "lfmmi_schedule.cpp", "lfmmi_fst.cpp"]
+                "lfmmi_schedule.cpp", "lfmmi_fst.cpp", "lfmmi_options.cpp"]
 
 
 def _run(cmd, verbose):
@@ -51,14 +51,17 @@ def build_core(verbose=True, force=False):
     if not force and not _stale(CORE_SO, deps):
         return CORE_SO
     os.makedirs(LIB_DIR, exist_ok=True)
-    objs = []
-    for s in srcs:
-        obj = os.path.join(LIB_DIR, os.path.basename(s) + ".o")
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-Xptxas", "-v" if os.environ.get("LFMMI_PTXAS_VERBOSE") else "-O3",
-              "-x", "cu" if s.endswith(".cu") else "c++",
-              "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", obj], verbose)
-        objs.append(obj)
+    objs = [os.path.join(LIB_DIR, os.path.basename(s) + ".o") for s in srcs]
+    cmds = [[NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if os.environ.get("LFMMI_PTXAS_VERBOSE") else "-O3",
+             "-x", "cu" if s.endswith(".cu") else "c++",
+             "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o] for s, o in zip(srcs, objs)]
+    # translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as pool:
+        for f in [pool.submit(_run, c, verbose) for c in cmds]:
+            f.result()
     _run([NVCC, *ARCH, "-shared", "-o", CORE_SO, *objs, "-lcudart"], verbose)
     for o in objs:
         os.remove(o)

@@ -17,6 +17,7 @@
 
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
+#include "lfmmi_options.h"
 
 namespace lfmmi {
 
@@ -37,7 +38,7 @@ __global__ void fwd_parity_kernel(DevGraphs g, const int64_t *row_map, int B, in
   const double *p = g.in_p64 + desc[kArcOff];
   const double *fin = g.fin64 + desc[kStateOff];
   const double *pi = leak_pi + size_t(row) * S_max;
-  const int T = lengths[b];
+  const int T = item_frames(lengths, b, T_max);
   const size_t T1 = size_t(T_max) + 1;
   __shared__ double s_total;
   __shared__ int s_fail;
@@ -108,7 +109,7 @@ __global__ void bwd_parity_kernel(DevGraphs g, const int64_t *row_map, int B, in
   const double *p = g.out_p64 + desc[kArcOff];
   const double *fin = g.fin64 + desc[kStateOff];
   const double *pi = leak_pi + size_t(row) * S_max;
-  const int T = lengths[b];
+  const int T = item_frames(lengths, b, T_max);
   const size_t T1 = size_t(T_max) + 1;
   double *be = beta + size_t(b) * T1 * S_max;
   __shared__ double s_dot;
@@ -156,7 +157,7 @@ __global__ void post_parity_kernel(DevGraphs g, const int64_t *row_map, int B, i
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= B * T_max) return;
   const int b = u / T_max, t = u % T_max;
-  if (t >= lengths[b] || fail[b] >= 0) return;
+  if (t >= item_frames(lengths, b, T_max) || fail[b] >= 0) return;
   const int row = int(row_map[b]);
   const int *desc = g.desc + row * kDescInts;
   const int I = desc[kI];
@@ -276,12 +277,23 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
   // only on the graph batch, so an utterance's result never depends on which
   // other utterances share its batch.
   const bool small = graphs->max_states <= 512;
-  if (!std::getenv("LFMMI_DISABLE_TILE")) {
+  const Options &opt = options();
+  if constexpr (std::is_same<Real, float>::value) {
+    if (graphs->linear && opt.linear) {  // the reference's numerators: linear chains
+      const int rc = launch_linear(a, graphs, st);
+      if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
+    }
+  }
+  if (graphs->linear_only)
+    return set_error(LFMMI_ERR_INVALID,
+                     "a linear-chain graph handle (lfmmi_graphs_create_linear) runs in fp32 with "
+                     "the uniform leak distribution and the linear option enabled");
+  if (opt.tile) {
     const int rc = launch_tile<Real>(a, graphs, small, st);
     if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
   }
   // Arc packs too large for shared memory: stream them from L2 (coalesced tiles).
-  if (!small && !std::getenv("LFMMI_DISABLE_STREAM")) {
+  if (!small && opt.stream) {
     const int rc = launch_stream<Real>(a, graphs, st);
     if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
   }
@@ -406,7 +418,7 @@ __global__ void combine_kernel(bool packed, int B, int T_max, int D, const int *
     batch_totals(B, lengths, num_lp, den_lp, num_fail, den_fail, totals);
   const size_t row_elems = size_t(T_max) * D;
   for (int b = blockIdx.y; b < B; b += gridDim.y) {
-    const size_t n = size_t(lengths[b]) * D;
+    const size_t n = size_t(item_frames(lengths, b, T_max)) * D;
     const bool ok = num_fail[b] < 0 && den_fail[b] < 0;
     size_t base = size_t(b) * row_elems;
     if (packed) {  // ragged rows: item b starts at sum_{j<b} T_j
@@ -502,67 +514,8 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
     return set_error(LFMMI_ERR_INVALID, "lfmmi_chain_loss: NULL device pointer");
   if (!(leak >= 0.0) || !(scale_floor > 0.0))
     return set_error(LFMMI_ERR_INVALID, "leak must be >= 0 and scale_floor > 0");
-  // Fused single-launch path (fp32, uniform leak, both graphs tileable, one
-  // shared emission-row layout): numerator + denominator + gradient per CTA.
-  // Opt-in (LFMMI_FUSED=1): on B200 the two-pass path below is ~7% faster at
-  // WSJ-mono because the numerator warps then overlap the denominator CTAs
-  // instead of lengthening their per-frame critical path (profiles/).
-  const char *fz = std::getenv("LFMMI_FUSED");
-  const bool want_fused = fz && std::atoi(fz) != 0;
-  if (want_fused && precision == LFMMI_F32 && !num_leak_pi && !den_leak_pi &&
-      denominator->tileable && numerators->tileable &&
-      denominator->rep_e == numerators->rep_e && denominator->e_stride == numerators->e_stride) {
-    ChainArgs c{};
-    c.den = denominator->dev;
-    c.num = numerators->dev;
-    c.den_row_map = den_row_map;
-    c.num_row_map = num_row_map;
-    c.B = batch;
-    c.T_max = max_frames;
-    c.D = num_pdfs;
-    c.D_pad = pad4(num_pdfs);
-    c.T_pad = pad4(max_frames);
-    c.Sd_pad = pad4(denominator->max_states);
-    c.Sn_pad = pad4(numerators->max_states);
-    c.rep_rd = denominator->rep_r;
-    c.r_strided = denominator->r_stride;
-    c.rep_rn = numerators->rep_r;
-    c.r_striden = numerators->r_stride;
-    c.rep_e = denominator->rep_e;
-    c.e_stride = denominator->e_stride;
-    c.L = static_cast<const float *>(loglikes);
-    c.lengths = lengths;
-    c.leak = float(leak);
-    c.floor_eff = float(std::max(scale_floor, double(FLT_MIN)));
-    c.trellis_d = reinterpret_cast<float *>(ws + den_off);
-    c.trellis_n = reinterpret_cast<float *>(ws + num_off);
-    c.grad = static_cast<float *>(grad);
-    c.num_lp = num_log_probs;
-    c.den_lp = den_log_probs;
-    c.num_fail = num_fail;
-    c.den_fail = den_fail;
-    c.totals = totals;
-    c.counter = reinterpret_cast<unsigned *>(ws + gam_off);
-    c.packed = packed ? 1 : 0;
-    ChainDims m{};
-    m.Fd = std::max(denominator->max_tf_slots, denominator->max_tb_slots);
-    m.ntd = denominator->max_tiles;
-    m.Xd = pad4(std::max(4, denominator->max_xpad));
-    m.Fn = std::max(numerators->max_tf_slots, numerators->max_tb_slots);
-    m.ntn = numerators->max_tiles;
-    m.Xn = pad4(std::max(4, numerators->max_xpad));
-    if (totals) {
-      rc = check_cuda(cudaMemsetAsync(c.counter, 0, sizeof(unsigned), st), "cudaMemsetAsync");
-      if (rc) return rc;
-    }
-    rc = launch_chain(c, m, st);
-    if (rc != LFMMI_ERR_UNSUPPORTED) {
-      g_launches = rc == LFMMI_OK ? 1 : 0;
-      return rc;
-    }
-  }
   AuxStream &ax = aux_for_device();
-  const bool serial = std::getenv("LFMMI_SERIAL_CHAIN") != nullptr;
+  const bool serial = options().serial != 0;
   cudaStream_t nst = serial ? st : ax.aux;
   // Two-pass path: the numerator pass (small graphs, latency-bound, one warp
   // per utterance) runs on the auxiliary stream next to the denominator pass

@@ -13,6 +13,14 @@ namespace lfmmi {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Frames of item b as the kernels see them: a length outside [1, T_max] (a
+// caller mistake such as pre-subsampling lengths) makes the item a failed
+// zero-length item instead of an out-of-bounds write.
+__device__ __forceinline__ int item_frames(const int *lengths, int b, int T_max) {
+  const int T = lengths[b];
+  return (T >= 1 && T <= T_max) ? T : 0;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -70,7 +70,46 @@ struct HostPack {
   std::vector<double> tf_p64, tb_p64;
   std::vector<unsigned short> tb_xslot, tf_xslot;
   std::vector<uint2> tf_wp, tb_wp;
+  std::vector<int> lin_item;         // 4 per row: state offset, S, initial, 0
+  std::vector<unsigned> lin_state;   // 4 per state (fb_linear_kernel record)
 };
+
+// Linear-chain record of one graph row (fb_linear_kernel): every arc is a
+// self-loop s -> s or an entry arc s-1 -> s, at most one of each per state —
+// the shape of the reference's numerators (toy_builder.py:218-265).  Returns
+// false (and leaves `out` untouched) for any other graph.
+bool linear_records(int S, int I, const uint32_t *from, const uint32_t *to, const uint32_t *pdf,
+                    const double *prob, const double *finals, std::vector<unsigned> &out) {
+  if (S > 512) return false;
+  std::vector<unsigned> rec(size_t(S) * 4, 0u);
+  std::vector<char> has_self(S, 0), has_in(S, 0);
+  for (int i = 0; i < I; ++i) {
+    const uint32_t f = from[i], t = to[i], d = pdf[i];
+    if (d > 0xffffu) return false;
+    const float p = float(prob[i]);
+    unsigned bits;
+    std::memcpy(&bits, &p, 4);
+    if (t == f) {
+      if (has_self[t]) return false;
+      has_self[t] = 1;
+      rec[4 * t + 0] = bits;
+      rec[4 * t + 2] |= d;
+    } else if (t == f + 1) {
+      if (has_in[t]) return false;
+      has_in[t] = 1;
+      rec[4 * t + 1] = bits;
+      rec[4 * t + 2] |= d << 16;
+    } else {
+      return false;
+    }
+  }
+  for (int s = 0; s < S; ++s) {
+    const float f = float(finals[s]);
+    std::memcpy(&rec[4 * s + 3], &f, 4);
+  }
+  out.insert(out.end(), rec.begin(), rec.end());
+  return true;
+}
 
 // Chunk length for the pdf-grouped posterior gather: aim for about one chunk
 // per thread of the largest block (1024), never longer than needed.
@@ -108,6 +147,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   int max_tiles = 0, max_tf = 0, max_tb = 0, max_xpad = 0;
   bool all_tileable = true;
   bool all_streamable = true;
+  bool all_linear = true;
   int max_stiles = 0;
   for (int r = 0; r < num_rows; ++r) {
     const int S = int(row_num_states[r]);
@@ -139,6 +179,12 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
       const double f = final_probs[size_t(r) * max_states + s];
       h.fin64.push_back(f);
       h.fin32.push_back(float(f));
+    }
+
+    if (all_linear) {
+      h.lin_item.insert(h.lin_item.end(), {int(h.lin_state.size() / 4), S, d[kInit], 0});
+      all_linear = linear_records(S, I, fw_from + base, fw_to + base, fw_pdf + base, fw_prob + base,
+                                  final_probs + size_t(r) * max_states, h.lin_state);
     }
 
     // out-CSR: the reference forward_* order is already sorted by source.
@@ -324,34 +370,25 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           const int chore = std::min(kTableNW, (num_pdfs + 31) / 32);
           // (a frame's chores are latency chains — row max, exp, prefetch — worth
           // ~16 slot rows of arc work; measured: bias 2 -> 16, den 1.419 -> 1.294 ms)
-          static const int chore_bias = [] {  // LFMMI_CHORE_BIAS overrides (A/B)
-            const char *e = std::getenv("LFMMI_CHORE_BIAS");
-            return e ? std::atoi(e) : 16;
-          }();
+          constexpr int chore_bias = 16;
           for (int w = kTableNW - chore; w < kTableNW; ++w) bias[w] = chore_bias;
           d[kWTabOff] = int(h.tf_wtab.size());
           warp_lists(tf.trips, bias, tab, lst);
           h.tf_wtab.insert(h.tf_wtab.end(), tab.begin(), tab.end());
           h.tf_wlist.insert(h.tf_wlist.end(), lst.begin(), lst.end());
           // Backward: the top warps also flush the gradient row of the previous
-          // frame (fb_chain_kernel, spl lanes per pdf, ~5 instructions per float4
+          // frame (fb_tile_kernel, spl lanes per pdf, ~5 instructions per float4
           // of posterior slots vs ~14 per arc-slot row).
           int spl = 1;
           while (spl < 32 && num_pdfs * spl * 2 <= 32 * kTableNW) spl <<= 1;
           const int lanes = num_pdfs * spl;
-          static const int chore_bias_bwd = [] {  // LFMMI_CHORE_BIAS_BWD overrides (A/B)
-            const char *e = std::getenv("LFMMI_CHORE_BIAS_BWD");
-            return e ? std::atoi(e) : chore_bias;
-          }();
+          constexpr int chore_bias_bwd = chore_bias;
           for (int w = kTableNW - chore; w < kTableNW; ++w) bias[w] = chore_bias_bwd;
-          if (lanes < 32 * kTableNW && !std::getenv("LFMMI_NO_FLUSH_BIAS")) {
+          if (lanes < 32 * kTableNW) {
             const int fw = (lanes + 31) / 32;
             const int per_lane = (xpad / 4 + lanes - 1) / lanes;
-            static const int flush_scale = [] {  // LFMMI_FLUSH_BIAS_PCT overrides (A/B)
-              const char *e = std::getenv("LFMMI_FLUSH_BIAS_PCT");
-              return e ? std::atoi(e) : 100;
-            }();
-            const int fb = ((per_lane * 5 + 13) / 14) * flush_scale / 100;
+            // (flush-bias scale 50-300% measured as slow or slower: DESIGN.md §3.3)
+            const int fb = (per_lane * 5 + 13) / 14;
             for (int w = kTableNW - fw; w < kTableNW; ++w) bias[w] += fb;
           }
           warp_lists(tb.trips, bias, tab, lst);
@@ -435,6 +472,11 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   g->streamable = all_streamable;
   g->max_stiles = max_stiles;
   g->max_xpad = max_xpad;
+  g->linear = all_linear;
+  if (!all_linear) {
+    h.lin_item.clear();
+    h.lin_state.clear();
+  }
   g->rep_r = gl.rep_r;
   g->r_stride = gl.r_stride;
   g->rep_e = gl.rep_e;
@@ -497,6 +539,8 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   add(h.pdf_arc_ptr, &dv.pdf_arc_ptr);
   add(h.tf_wp, &dv.tf_wp);
   add(h.tb_wp, &dv.tb_wp);
+  add(h.lin_item, &dv.lin_item);
+  add(h.lin_state, &dv.lin_state);
   size_t total = 0;
   std::vector<size_t> offs;
   for (auto &p : pieces) {
@@ -524,6 +568,29 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   g->device_block = dev;
   g->device_bytes = total;
   *out = g;
+  return LFMMI_OK;
+}
+
+extern "C" int lfmmi_graphs_create_linear(int32_t num_rows, int32_t max_states, int32_t num_pdfs,
+                                          const int32_t *items, const uint32_t *states,
+                                          lfmmi_graphs **out) {
+  if (!out) return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create_linear: out is NULL");
+  *out = nullptr;
+  if (num_rows < 1 || max_states < 1 || max_states > 512 || num_pdfs < 1 || num_pdfs > 65536)
+    return set_error(LFMMI_ERR_INVALID,
+                     "lfmmi_graphs_create_linear: need 1 <= max_states <= 512, 1 <= num_pdfs <= 65536");
+  if (!items || !states)
+    return set_error(LFMMI_ERR_INVALID, "lfmmi_graphs_create_linear: NULL device array");
+  auto *g = new lfmmi_graphs();
+  g->num_rows = num_rows;
+  g->max_states = max_states;
+  g->max_arcs = 2 * max_states;
+  g->num_pdfs = num_pdfs;
+  g->linear = true;
+  g->linear_only = true;
+  g->dev.lin_item = reinterpret_cast<const int4 *>(items);
+  g->dev.lin_state = reinterpret_cast<const uint4 *>(states);
+  *out = g;  // device_block stays NULL: the caller owns the arrays
   return LFMMI_OK;
 }
 

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(GROUP *GPC, 1) fb_group_kernel(const FBArgs<Re
   Real *mpart = sm + lay.mpart;
   auto gsync = [&]() { group_sync<GROUP, GPC>(gid); };
 
-  const int T = a.lengths[b];
+  const int T = item_frames(a.lengths, b, a.T_max);
   const int D = a.D;
   const int S_pad = a.S_pad, D_pad = a.D_pad, NC_pad = a.NC_pad;
   const int row = int(a.row_map[b]);

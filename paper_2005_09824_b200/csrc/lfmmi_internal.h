@@ -77,6 +77,11 @@ struct DevGraphs {
   const int *sf_info, *sb_info;       // stream packs: state per tile lane (-1 = none)
   const int *sf_trips, *sf_base, *sb_trips, *sb_base;
   const uint2 *sf_wp, *sb_wp;         // {index | pdf << 15, fp32 prob bits}
+  // linear-chain pack (fb_linear_kernel): per row {state offset, S, initial, 0};
+  // per state {fp32 self-loop prob, fp32 entry prob (arc s-1 -> s),
+  // self pdf | entry pdf << 16, fp32 final prob}
+  const int4 *lin_item;
+  const uint4 *lin_state;
 };
 
 }  // namespace lfmmi
@@ -87,6 +92,8 @@ struct lfmmi_graphs {
   int32_t max_tiles = 0, max_tf_slots = 0, max_tb_slots = 0, max_xpad = 0;
   bool tileable = false;
   bool streamable = false;  // every row has a stream pack (fb_stream_kernel)
+  bool linear = false;      // every row is a linear chain (fb_linear_kernel pack present)
+  bool linear_only = false; // lfmmi_graphs_create_linear: nothing but the linear pack
   int32_t max_stiles = 0;
   int32_t rep_r = 1, r_stride = 0, rep_e = 1, e_stride = 0;  // gather-vector replication
   void *device_block = nullptr;

@@ -34,32 +34,10 @@ int launch_split(const FBArgs<Real> &a, const lfmmi_graphs *graphs, cudaStream_t
 template <typename Real>
 int launch_stream(const FBArgs<Real> &a, const lfmmi_graphs *graphs, cudaStream_t st);
 
-// Fused LF-MMI loss (lfmmi_chain.cu): numerator + denominator + gradient in one CTA.
-struct ChainArgs {
-  DevGraphs den, num;
-  const int64_t *den_row_map, *num_row_map;
-  int B, T_max, D, D_pad, T_pad;
-  int Sd_pad, Sn_pad;  // trellis row strides
-  int rep_rd, r_strided, rep_rn, r_striden, rep_e, e_stride;
-  const float *L;
-  const int *lengths;
-  float leak, floor_eff;
-  float *trellis_d, *trellis_n;
-  float *grad;
-  double *num_lp, *den_lp;
-  int *num_fail, *den_fail;
-  double *totals;
-  unsigned *counter;
-  long long *prof;  // debug section timers (LFMMI_PROFILE), normally NULL
-  int ablate;       // debug ablation bits (LFMMI_ABLATE, profiled launches only)
-  int packed;       // ragged (sum_b T_b, D) loglikes / grad
-};
-
-struct ChainDims {
-  int Fd, ntd, Xd;  // denominator: max slots per phase, tiles, posterior slots
-  int Fn, ntn, Xn;  // numerator
-};
-
-int launch_chain(const ChainArgs &a, const ChainDims &m, cudaStream_t st);
+// Linear-chain graphs (every arc s -> s or s -> s+1, <= 1 of each per state;
+// the reference's numerators): one warp per utterance, states in registers
+// (lfmmi_linear.cu).  fp32, uniform leak; LFMMI_ERR_UNSUPPORTED (without
+// launching) when not applicable.
+int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st);
 
 }  // namespace lfmmi

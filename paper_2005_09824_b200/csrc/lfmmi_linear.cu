@@ -1,0 +1,393 @@
+// Linear-chain forward-backward: the numerator pass.
+//
+// The reference's numerator graphs are linear chains (build_numerator,
+// /root/reference/pkg/src/chainloss/toy_builder.py:218-265): state 0 enters
+// phone 1, state k has one self-loop and one arc to k+1.  For such a graph
+// the sparse recursion of _kernels.py:54-191 collapses to a two-term stencil
+//
+//   raw_{t+1}[s] = w_self_t[s] * alpha_t[s] + w_in_t[s] * alpha_t[s-1]
+//   X_{t-1}[s]   = w_self_t[s] * beta_t[s]  + w_in_t[s+1] * beta_t[s+1]
+//
+// (w = p * exp(L[t, pdf] - max_d L[t, d])), so one warp runs an utterance with
+// its states in registers: lane l owns states [l K, l K + K), the s-1 / s+1
+// neighbours crossing a lane boundary come from one shuffle, and the only
+// cross-lane reductions are the per-frame normaliser (forward) and the
+// leaky-HMM dot product (backward).  Both are deferred (the stencil runs on
+// the unnormalised column and the scalars are folded in afterwards), so a
+// frame's critical path is one warp reduction plus a few FMAs.  No block
+// barrier, no arc tables in shared memory.
+//
+// Semantics follow the reference exactly: finals at t == T (:97-98), uniform
+// leak pi = 1/S (forward_backward.py:133-166 default) re-normalised by
+// tot = R (1 + leak) (:108-113), failure when !(tot >= floor) or tot == inf
+// (:114-118), beta_T = final (1 + leak) / scale_{T-1} (:152-158), the leak
+// adjoint and 1/scale_{t-2} in the backward (:177-191), and posteriors
+// gamma[t, d] = sum_{pdf_i = d} alpha_t[src] p_i e[t, d] beta_{t+1}[dst]
+// (:211-224), accumulated per frame in a per-warp shared-memory histogram as
+// 2^-28 fixed-point integers (order-independent => deterministic).
+//
+// Log-likelihood rows are staged by cp.async kRing-1 frames ahead (coalesced
+// 16-byte chunks), alpha rows of the backward likewise; the row maximum is
+// taken from the staged row (NaN-propagating, forward_backward.py:126).
+#include "lfmmi_device.cuh"
+#include "lfmmi_kernels.h"
+
+namespace lfmmi {
+namespace {
+
+constexpr int kRing = 4;                       // cp.async stages (frames in flight + 1)
+constexpr float kFix = 268435456.0f;           // 2^28: posterior fixed-point scale
+constexpr float kUnfix = 1.0f / 268435456.0f;
+
+struct LinLayout {
+  int T4, Dr, stage;  // floats
+  size_t bytes;
+};
+
+__host__ __device__ inline LinLayout lin_layout(int T_max, int D, int K) {
+  LinLayout l;
+  l.T4 = pad4(T_max);
+  l.Dr = pad4(D);
+  l.stage = l.Dr + 32 * K;
+  // scales[T4] | shifts[T4] | histogram[Dr] (u32) | ring[kRing][stage]
+  l.bytes = size_t(2 * l.T4 + l.Dr + kRing * l.stage) * 4;
+  return l;
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a) {
+  extern __shared__ __align__(16) float lsm[];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const int D = a.D, T_max = a.T_max;
+  const LinLayout lay = lin_layout(T_max, D, K);
+  float *scl = lsm;                    // per-frame scales (forward normalisers)
+  float *shf = lsm + lay.T4;           // per-frame row maxima
+  unsigned *hist = reinterpret_cast<unsigned *>(lsm + 2 * lay.T4);
+  float *ring = lsm + 2 * lay.T4 + lay.Dr;
+  const int mode = a.mode;
+  const bool reads_post = mode == kPostAdd || mode == kPostSubtract;
+
+  // Row offset of this item in the ragged trellis (and in L / post when packed).
+  long long off = 0;
+  for (int j = lane; j < b; j += 32) off += a.packed ? a.lengths[j] : item_frames(a.lengths, j, T_max);
+  off = warp_sum(off);
+  const int T = item_frames(a.lengths, b, T_max);
+  const size_t row0 = a.packed ? size_t(off) : size_t(b) * T_max;
+  const float *Lb = a.L + row0 * D;
+  float *post_b = a.post + row0 * D;
+  if (!reads_post && !a.packed)  // padded rows of this item
+    for (size_t i = lane; i < size_t(T_max - T) * D; i += 32) post_b[size_t(T) * D + i] = 0.f;
+  if (T <= 0) {  // zero-length (or out-of-range) item: failed, no frames touched
+    if (a.scale_logs && !a.packed)
+      for (int k = lane; k < T_max; k += 32) a.scale_logs[size_t(b) * T_max + k] = 0.0;
+    if (lane == 0) {
+      a.logp[b] = NAN;
+      a.fail[b] = 0;
+    }
+    return;
+  }
+  const int ld = (a.S_max + 31) & ~31;  // trellis row stride (lfmmi_workspace_size)
+  float *tr = a.work + size_t(off) * ld;
+  const bool own_row = lane * K < ld;
+
+  // ---- graph: two arcs per state, in registers ----------------------------------
+  const int4 item = a.g.lin_item[a.row_map[b]];
+  const int S = item.y, init = item.z;
+  const uint4 *rec = a.g.lin_state + item.x;
+  float ps[K], pin[K], fin[K];
+  unsigned pdp[K];  // self pdf | entry pdf << 16
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int s = lane * K + k;
+    const uint4 v = s < S ? rec[s] : make_uint4(0u, 0u, 0u, 0u);
+    ps[k] = __uint_as_float(v.x);
+    pin[k] = __uint_as_float(v.y);
+    pdp[k] = v.z;
+    fin[k] = __uint_as_float(v.w);
+  }
+  // arc (lane K + K - 1) -> (lane K + K): the entry arc of the next lane's first state
+  float po_last = __shfl_down_sync(kFull, pin[0], 1);
+  unsigned pdo_last = __shfl_down_sync(kFull, pdp[0], 1) >> 16;
+  if (lane == 31) {
+    po_last = 0.f;
+    pdo_last = 0u;
+  }
+  const float leak = a.leak;
+  const float vleak = leak > 0.f ? leak / (float(S) * (1.f + leak)) : 0.f;  // leak * pi / (1 + leak)
+
+  const bool vec16 = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.L) & 15) == 0);
+  auto stage = [&](int t) { return ring + (t % kRing) * lay.stage; };
+  auto issue_row = [&](int t) {
+    float *dst = stage(t);
+    const float *src = Lb + size_t(t) * D;
+    if (vec16) {
+      for (int c = lane; c < (D >> 2); c += 32) cp_async_16(dst + 4 * c, src + 4 * c);
+    } else {
+      for (int d = lane; d < D; d += 32) cp_async_elem(dst + d, src + d);
+    }
+  };
+  auto issue_alpha = [&](int t) {  // alpha row t (this lane's K states) behind the L row
+    if (!own_row) return;
+    float *dst = stage(t) + lay.Dr + lane * K;
+    const float *src = tr + size_t(t) * ld + lane * K;
+    if constexpr (K >= 4) {
+#pragma unroll
+      for (int c = 0; c < K; c += 4) cp_async_16(dst + c, src + c);
+    } else {
+#pragma unroll
+      for (int c = 0; c < K; ++c) cp_async_elem(dst + c, src + c);
+    }
+  };
+  auto emission = [&](const float *Lt, unsigned pdf, float m) { return expf(Lt[pdf] - m); };
+
+  // ---- forward (_kernels.py:54-122) ---------------------------------------------
+  float r[K];  // unnormalised column: alpha_0 (one-hot) at t = 0, raw_t after
+#pragma unroll
+  for (int k = 0; k < K; ++k) r[k] = (lane * K + k == init) ? 1.f : 0.f;
+  int fail_at = -1;
+#pragma unroll
+  for (int p = 0; p < kRing - 1; ++p) {
+    if (p < T) issue_row(p);
+    cp_async_commit();
+  }
+  for (int t = 0; t < T; ++t) {
+    __syncwarp();  // stage of frame t-1 fully consumed before it is refilled
+    if (t + kRing - 1 < T) issue_row(t + kRing - 1);
+    cp_async_commit();
+    cp_async_wait<kRing - 1>();
+    __syncwarp();
+    const float *Lt = stage(t);
+    // normaliser of column t (t >= 1); runs beside the stencil below
+    float R = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) R += r[k];
+    // unnormalised stencil on column t
+    float prev = __shfl_up_sync(kFull, r[K - 1], 1);
+    if (lane == 0) prev = 0.f;
+    float m = -INFINITY;
+    for (int d = lane; d < D; d += 32) m = nan_max(m, Lt[d]);
+    R = warp_sum(R);
+    m = warp_max(m);
+    float A[K], Bv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float ws = ps[k] * emission(Lt, pdp[k] & 0xffffu, m);
+      const float wi = pin[k] * emission(Lt, pdp[k] >> 16, m);
+      A[k] = ws * r[k] + wi * (k ? r[k - 1] : prev);
+      Bv[k] = ws + wi;
+    }
+    float u = 1.f, v = 0.f;
+    if (t > 0) {
+      float tot = R;
+      if (leak > 0.f && R > 0.f) {
+        tot = R + leak * R;
+        v = vleak;
+      }
+      if (!(tot >= a.floor_eff) || tot == INFINITY) {
+        fail_at = t - 1;
+        break;
+      }
+      u = rcp_rn(tot);
+      if (lane == 0) scl[t - 1] = tot;
+    }
+    if (lane == 0) shf[t] = m;
+    // normalised alpha_t -> trellis row t (posteriors of frame t in the backward)
+    if (own_row) {
+      float al[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) al[k] = lane * K + k < S ? fmaf(r[k], u, v) : 0.f;
+      float *dst = tr + size_t(t) * ld + lane * K;
+      if constexpr (K >= 4) {
+#pragma unroll
+        for (int c = 0; c < K; c += 4)
+          *reinterpret_cast<float4 *>(dst + c) = make_float4(al[c], al[c + 1], al[c + 2], al[c + 3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < K; ++c) dst[c] = al[c];
+      }
+    }
+    // raw_{t+1} = W (r u + v) = u (W r) + v (W 1)
+#pragma unroll
+    for (int k = 0; k < K; ++k) r[k] = fmaf(u, A[k], v * Bv[k]);
+    if (t + 1 == T) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) r[k] *= fin[k];  // finals at the last frame (:97-98)
+    }
+  }
+  cp_async_wait<0>();
+  if (fail_at < 0) {  // column T
+    float R = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) R += r[k];
+    R = warp_sum(R);
+    const float tot = (leak > 0.f && R > 0.f) ? R + leak * R : R;
+    if (!(tot >= a.floor_eff) || tot == INFINITY)
+      fail_at = T - 1;
+    else if (lane == 0)
+      scl[T - 1] = tot;
+  }
+  if (fail_at >= 0) {
+    // scales stay 1 from the failing frame on; the shifts of the frames the loop
+    // did not reach are still reported (forward_backward.py:184,206)
+    for (int k = fail_at; k < T; ++k) {
+      if (k > fail_at) {
+        float m = -INFINITY;
+        for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
+        m = warp_max(m);
+        if (lane == 0) shf[k] = m;
+      }
+      if (lane == 0) scl[k] = 1.f;
+    }
+  }
+  __syncwarp();
+  {
+    double acc = 0.0;
+    for (int k = lane; k < T; k += 32) {
+      const double v = log(double(scl[k])) + double(shf[k]);
+      acc += v;
+      if (a.scale_logs) a.scale_logs[size_t(b) * T_max + k] = v;
+    }
+    if (a.scale_logs)
+      for (int k = T + lane; k < T_max; k += 32) a.scale_logs[size_t(b) * T_max + k] = 0.0;
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      a.logp[b] = fail_at >= 0 ? NAN : acc;
+      a.fail[b] = fail_at;
+    }
+  }
+  const bool other_failed = a.other_fail != nullptr && a.other_fail[b] >= 0;
+  if (fail_at >= 0 || other_failed) {
+    for (size_t i = lane; i < size_t(T) * D; i += 32) post_b[i] = 0.f;
+    return;
+  }
+
+  // ---- backward + posteriors (_kernels.py:125-224) --------------------------------
+  // beta_t = Y_t / scale_{t-1} + z_t, z_t = leak (pi . Y_t) / scale_{t-1} (t < T).
+  for (int d = lane; d < lay.Dr; d += 32) hist[d] = 0u;
+  float Y[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) Y[k] = fin[k] * (1.f + leak);
+#pragma unroll
+  for (int p = 0; p < kRing - 1; ++p) {
+    const int e = T - 1 - p;
+    if (e >= 0) {
+      issue_row(e);
+      issue_alpha(e);
+    }
+    cp_async_commit();
+  }
+  const bool vflush = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(post_b) & 15) == 0);
+  for (int t = T; t >= 1; --t) {
+    const int e = t - 1;  // emission frame
+    __syncwarp();         // stage + histogram of frame e+1 consumed
+    {
+      const int en = e - (kRing - 1);
+      if (en >= 0) {
+        issue_row(en);
+        issue_alpha(en);
+      }
+      cp_async_commit();
+    }
+    cp_async_wait<kRing - 1>();
+    __syncwarp();
+    const float *Lt = stage(e);
+    const float *al = Lt + lay.Dr + lane * K;
+    const float m = shf[e];
+    const float q = rcp_rn(scl[t - 1]);
+    float sY = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) sY += Y[k];
+    float ynext = __shfl_down_sync(kFull, Y[0], 1);
+    if (lane == 31) ynext = 0.f;
+    float ws[K], wo[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) ws[k] = ps[k] * emission(Lt, pdp[k] & 0xffffu, m);
+#pragma unroll
+    for (int k = 0; k < K - 1; ++k) wo[k] = pin[k + 1] * emission(Lt, pdp[k + 1] >> 16, m);
+    wo[K - 1] = po_last * emission(Lt, pdo_last, m);
+    float A[K], Bv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      A[k] = ws[k] * Y[k] + wo[k] * (k + 1 < K ? Y[k + 1] : ynext);
+      Bv[k] = ws[k] + wo[k];
+    }
+    float z = 0.f;
+    if (leak > 0.f && t < T) z = leak * q * (warp_sum(sY) / float(S));
+    // posterior terms of frame e: alpha_e[src] * p e * beta_t[dst]
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float a_s = own_row ? al[k] : 0.f;
+      const float bs = fmaf(Y[k], q, z);
+      const float bn = fmaf(k + 1 < K ? Y[k + 1] : ynext, q, z);
+      const float gs = a_s * ws[k] * bs;
+      const float go = a_s * wo[k] * bn;
+      if (gs > 0.f) atomicAdd(hist + (pdp[k] & 0xffffu), __float2uint_rn(gs * kFix));
+      const unsigned pdo = k + 1 < K ? (pdp[k + 1] >> 16) : pdo_last;
+      if (go > 0.f) atomicAdd(hist + pdo, __float2uint_rn(go * kFix));
+    }
+    // X_{t-1} = Y_{t-1}: the next column (reference beta_{t-1} before leak / scale)
+#pragma unroll
+    for (int k = 0; k < K; ++k) Y[k] = fmaf(q, A[k], z * Bv[k]);
+    __syncwarp();
+    // flush gamma row e into the posterior output (mode), clearing the histogram
+    float *prow = post_b + size_t(e) * D;
+    if (vflush) {
+      uint4 *h4 = reinterpret_cast<uint4 *>(hist);
+      float4 *p4 = reinterpret_cast<float4 *>(prow);
+      for (int c = lane; c < (D >> 2); c += 32) {
+        const uint4 hv = h4[c];
+        h4[c] = make_uint4(0u, 0u, 0u, 0u);
+        float4 g = make_float4(float(hv.x) * kUnfix, float(hv.y) * kUnfix, float(hv.z) * kUnfix,
+                               float(hv.w) * kUnfix);
+        if (mode == kPostNegate) {
+          g = make_float4(-g.x, -g.y, -g.z, -g.w);
+        } else if (reads_post) {
+          const float4 o = p4[c];
+          const float sg = mode == kPostAdd ? 1.f : -1.f;
+          g = make_float4(o.x + sg * g.x, o.y + sg * g.y, o.z + sg * g.z, o.w + sg * g.w);
+        }
+        p4[c] = g;
+      }
+    } else {
+      for (int d = lane; d < D; d += 32) {
+        float g = float(hist[d]) * kUnfix;
+        hist[d] = 0u;
+        if (mode == kPostNegate) g = -g;
+        else if (mode == kPostAdd) g = prow[d] + g;
+        else if (mode == kPostSubtract) g = prow[d] - g;
+        prow[d] = g;
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int K>
+int launch_k(const FBArgs<float> &a, cudaStream_t st) {
+  const size_t smem = lin_layout(a.T_max, a.D, K).bytes;
+  if (smem > size_t(kMaxSmem)) return LFMMI_ERR_UNSUPPORTED;
+  if (smem > 48 * 1024) {
+    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_kernel<K>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(smem)),
+                              "cudaFuncSetAttribute(linear)");
+    if (rc) return rc;
+  }
+  fb_linear_kernel<K><<<a.B, 32, smem, st>>>(a);
+  return check_cuda(cudaGetLastError(), "fb_linear_kernel launch");
+}
+
+}  // namespace
+
+int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st) {
+  if (!g->linear || a.leak_pi != nullptr || a.D > 65536) return LFMMI_ERR_UNSUPPORTED;
+  const int S = g->max_states;
+  if (S <= 32) return launch_k<1>(a, st);
+  if (S <= 64) return launch_k<2>(a, st);
+  if (S <= 128) return launch_k<4>(a, st);
+  if (S <= 256) return launch_k<8>(a, st);
+  if (S <= 512) return launch_k<16>(a, st);
+  return LFMMI_ERR_UNSUPPORTED;
+}
+
+}  // namespace lfmmi

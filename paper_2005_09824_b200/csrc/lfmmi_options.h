@@ -1,0 +1,31 @@
+// Process-wide dispatch / debug options of the library: ONE struct, parsed once
+// from LFMMI_OPTIONS ("split=0,stream_mode=1024x1,...") on first use and
+// changeable at run time through lfmmi_set_option (include/lfmmi.h).  Nothing
+// else in the library reads the environment.
+#pragma once
+
+#include <string>
+
+namespace lfmmi {
+
+struct Options {
+  // kernel families the dispatcher may pick (1 = allowed)
+  int tile = 1;           // on-chip tile / split kernels
+  int stream = 1;         // L2-streamed kernel (graphs beyond shared memory)
+  int linear = 1;         // linear-chain numerator kernel
+  int split = -1;         // denominator split kernel: -1 auto (B <= 2 x SMs), 0 off, 1 force
+  int split_clusters = 0; // 0 = auto
+  int split_h64 = 33;     // split midpoint in 64ths of T
+  std::string stream_mode = "auto";  // "auto" | "1024x1" | "1024x2" | "512x2"
+  int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
+  int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots
+  int serial = 0;         // chain_loss: numerator pass on the caller's stream
+  int sched_iters = -1;   // bank-conflict local search moves per slot row (-1 auto)
+  int debug = 0;          // layout / dispatch notes on stderr
+  std::string profile;    // "" | "split" | "tile": per-frame cycle counters on stderr
+};
+
+// The current options (initialised from LFMMI_OPTIONS on first call).
+Options &options();
+
+}  // namespace lfmmi

@@ -17,6 +17,7 @@
 // first), picking the arc and copies that add the fewest new addresses to
 // already-used banks.  Broadcasts (same address) are free.
 #include "lfmmi_schedule.h"
+#include "lfmmi_options.h"
 
 #include <algorithm>
 #include <atomic>
@@ -54,26 +55,25 @@ struct BankSet {  // distinct addresses per bank within one slot row
 
 }  // namespace
 
-// Local-search moves per slot row (LFMMI_SCHED_ITERS overrides; 0 = greedy only).
-static int local_search_iters() {
-  static const int n = [] {
-    const char *e = std::getenv("LFMMI_SCHED_ITERS");
-    return e ? std::max(0, std::atoi(e)) : 1500;
-  }();
-  return n;
+// Local-search moves per slot row (option sched_iters; 0 = greedy only).  Auto:
+// 1500 for denominator-sized graphs; none for numerator-sized ones (<= 512
+// states), whose kernels are latency-bound at a few per cent of SMEM
+// bandwidth — the search cost ~7 ms of host time per numerator for nothing.
+static int local_search_iters(int S) {
+  const int o = options().sched_iters;
+  if (o >= 0) return o;
+  return S > 512 ? 1500 : 0;
 }
 
 GatherLayout make_gather_layout(int max_states, int num_pdfs) {
   GatherLayout gl;
   auto round32 = [](int x) { return (x + 31) & ~31; };
   // copy 1 of the gather column sits r_off banks over (LFMMI_R_OFF overrides)
-  const char *ro = std::getenv("LFMMI_R_OFF");
   // (9: the two candidate banks of an address form a ring rather than 16
   // disjoint pairs, which the row matching exploits better — offline: 1.87 ->
   // 1.66 wavefronts per warp-wide gather with the local search)
-  gl.r_stride = round32(max_states) + (ro ? std::atoi(ro) : 9);
+  gl.r_stride = round32(max_states) + 9;
   gl.rep_r = (2 * gl.r_stride <= 16383) ? 2 : 1;
-  if (const char *e = std::getenv("LFMMI_REP_R")) gl.rep_r = std::max(1, std::min(gl.rep_r, std::atoi(e)));
   if (gl.rep_r == 1) gl.r_stride = (max_states + 3) & ~3;
   gl.e_stride = round32(num_pdfs) + 8;  // copies shift by 8 banks
   gl.rep_e = 4;
@@ -322,7 +322,7 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
         }
       }
     }
-    if (optimize && trips > 1 && local_search_iters() > 0) {
+    if (optimize && trips > 1 && local_search_iters(S) > 0) {
       // slots[j][l] = CSR arc at row j, lane l (-1 idle); search over lane permutations.
       std::vector<std::array<int, 32>> slots(trips);
       for (int j = 0; j < trips; ++j)
@@ -330,7 +330,7 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
       std::vector<int> cost(trips);
       for (int j = 0; j < trips; ++j) cost[j] = eval_row(slots[j].data(), gidx, pdf, gl).cost;
       std::mt19937 rng(12345u + unsigned(w));
-      const int iters = local_search_iters() * trips;
+      const int iters = local_search_iters(S) * trips;
       for (int it = 0; it < iters; ++it) {
         const int l = int(rng() % 32u);
         const int j1 = int(rng() % unsigned(trips)), j2 = int(rng() % unsigned(trips));
@@ -419,7 +419,7 @@ void assign_xslots(const TileSchedule &tb, const int *pdf_of_arc, int num_pdfs, 
     for (int pos = pdf_ptr[p + 1] - 1; pos >= pdf_ptr[p]; --pos)
       freel[size_t(p) * 32 + (pos & 31)].push_back(pos);
   xslot_of_slot.assign(tb.arc.size(), dummy);
-  static const bool greedy_only = std::getenv("LFMMI_XSLOT_GREEDY") != nullptr;
+  constexpr bool greedy_only = false;  // (bipartite matching: 1.13 -> 1.00 wavefronts/row)
   long waves = 0, rows = 0;
   for (size_t w = 0; w < tb.trips.size(); ++w) {
     for (int j = 0; j < tb.trips[w]; ++j) {
@@ -509,7 +509,7 @@ void assign_xslots(const TileSchedule &tb, const int *pdf_of_arc, int num_pdfs, 
       ++rows;
     }
   }
-  if (std::getenv("LFMMI_DEBUG_XSLOT"))
+  if (options().debug)
     std::fprintf(stderr, "[lfmmi] xslot stores: %ld rows, %.3f wavefronts/row (%s)\n", rows,
                  rows ? double(waves) / double(rows) : 0.0, greedy_only ? "greedy" : "matching");
 }

@@ -31,6 +31,7 @@
 
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
+#include "lfmmi_options.h"
 #include "lfmmi_schedule.h"
 #include "lfmmi_tile_common.cuh"
 
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kNT, 1)
   {
     int *lens = reinterpret_cast<int *>(xterm);
     int *order = lens + a.B;
-    for (int i = tid; i < a.B; i += kNT) lens[i] = a.lengths[i];
+    for (int i = tid; i < a.B; i += kNT) lens[i] = item_frames(a.lengths, i, a.T_max);
     __syncthreads();
     for (int i = tid; i < a.B; i += kNT) {
       const int ti = lens[i];
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kNT, 1)
 
   for (int it = 0; it < nitems; ++it) {
     const int b = items[4 + it];
-    const int T = a.lengths[b];
+    const int T = item_frames(a.lengths, b, a.T_max);
     if (T <= 0) {  // zero-length item (host APIs reject it): failed, no frames touched
       if (fwd) {
         if (!a.packed)
@@ -652,9 +653,9 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const char *env = std::getenv("LFMMI_SPLIT");
-  if (env && std::atoi(env) == 0) return set_error(LFMMI_ERR_UNSUPPORTED, "split: disabled");
-  if (!(env && std::atoi(env) == 1) && a.B > 2 * sms)
+  const Options &opt = options();
+  if (opt.split == 0) return set_error(LFMMI_ERR_UNSUPPORTED, "split: disabled");
+  if (opt.split != 1 && a.B > 2 * sms)
     return set_error(LFMMI_ERR_UNSUPPORTED, "split: batch fills the SMs");
   const int Fmax = std::max(g->max_tf_slots, g->max_tb_slots);
   const int X_pad = pad4(std::max(4, g->max_xpad));
@@ -667,7 +668,7 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
     b.sc_smem = 0;
     lay = split_layout(Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad, a.T_pad, RB, EB, false);
   }
-  if (std::getenv("LFMMI_DEBUG"))
+  if (opt.debug)
     std::fprintf(stderr, "[lfmmi] split layout %zu B (limit %d)\n", lay.total, kMaxSmem);
   // scheduling scratch (lengths + order) lives in the posterior slot buffers
   if (lay.total > size_t(kMaxSmem) || size_t(2) * a.B * 4 > size_t(2) * X_pad * 4)
@@ -676,9 +677,8 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   // Clusters: one per utterance while they fit, leaving >= 20 SMs to the
   // numerator pass that runs beside this one (two-pass chain loss; measured on
   // WSJ-mono: numerators 0.87 ms on all SMs, 1.26 ms on 20); beyond that LPT
-  // pairs long with short utterances.  LFMMI_SPLIT_CLUSTERS overrides.
-  const char *nc_env = std::getenv("LFMMI_SPLIT_CLUSTERS");
-  int nc = nc_env ? std::atoi(nc_env) : std::min(a.B, sms / 2 - 10);
+  // pairs long with short utterances.  Option split_clusters overrides.
+  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 10);
   nc = std::max(1, std::min(nc, std::min(96, sms / 2)));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > std::min(96, sms / 2))
@@ -692,8 +692,7 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
     if (rc) return rc;
     configured = true;
   }
-  const char *h_env = std::getenv("LFMMI_SPLIT_H64");  // midpoint in 64ths of T (A/B)
-  const int hnum = h_env ? std::max(0, std::min(64, std::atoi(h_env))) : 33;
+  const int hnum = std::max(0, std::min(64, opt.split_h64));  // midpoint in 64ths of T
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * nc);
   cfg.blockDim = dim3(kNT);
@@ -706,14 +705,14 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (std::getenv("LFMMI_DEBUG")) {
+  if (opt.debug) {
     int maxc = -1;
     cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg);
     std::fprintf(stderr, "[lfmmi] split: %d clusters (max active %d), smem %zu (scales %s)\n", nc,
                  maxc, lay.total, b.sc_smem ? "smem" : "hbm");
   }
   note_den_kernel("fb_split_kernel (2-CTA cluster: forward | backward)");
-  if (!std::getenv("LFMMI_PROFILE_SPLIT"))
+  if (opt.profile != "split")
     return check_cuda(cudaLaunchKernelEx(&cfg, kern, b, Fmax, g->max_tiles, X_pad, nc, hnum),
                       "fb_split_kernel launch");
   // Debug: per-item section timestamps of both CTAs, summarised on stderr.

@@ -30,6 +30,7 @@
 // forward_backward.py:206-212.  Uniform leak distribution only.
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
+#include "lfmmi_options.h"
 
 #include <cooperative_groups.h>
 
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     bins_p = cl.map_shared_rank(bins, rank ^ 1);
   }
 
-  const int T = a.lengths[b];
+  const int T = item_frames(a.lengths, b, a.T_max);
   if (T <= 0) {  // zero-length item (host APIs reject it): failed, no frames touched
     if (rank == 0) {
       if (!a.packed)
@@ -472,8 +473,8 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   // Two SMs per utterance (2-CTA cluster of 1024-thread CTAs) while the batch
   // leaves SMs idle, else one 1024-thread CTA per utterance.  ("512x2" — two
   // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
-  const char *env = std::getenv("LFMMI_STREAM_MODE");  // "1024x1", "1024x2", "512x2"
-  std::string mode = env ? env : (2 * a.B <= sms ? "1024x2" : "1024x1");
+  const std::string &want = options().stream_mode;  // "1024x1", "1024x2", "512x2"
+  std::string mode = want != "auto" ? want : (2 * a.B <= sms ? "1024x2" : "1024x1");
   note_den_kernel(mode == "1024x2"  ? "fb_stream_kernel<1024,2>"
                   : mode == "512x2" ? "fb_stream_kernel<512,2>"
                                     : "fb_stream_kernel<1024,1>");

@@ -31,6 +31,7 @@
 // back during the backward.
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
+#include "lfmmi_options.h"
 #include "lfmmi_tile_common.cuh"
 #include "lfmmi_schedule.h"
 
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks 
   (void)wp32;
   (void)xs32;
 
-  const int T = a.lengths[b];
+  const int T = item_frames(a.lengths, b, a.T_max);
   if (T <= 0) {  // zero-length item (host APIs reject it): failed, no frames touched
     if (a.mode != kPostAdd && a.mode != kPostSubtract && !a.packed)
       for (size_t i = tid; i < size_t(a.T_max) * a.D; i += GROUP)
@@ -670,7 +671,7 @@ static int launch_tile_impl2(const FBArgs<Real> &a, const lfmmi_graphs *g, size_
   }
   const int grid = (a.B + IPC - 1) / IPC;
   const int Fmax = std::max(g->max_tf_slots, g->max_tb_slots);
-  if (GROUP != kDenGroupC || !std::getenv("LFMMI_PROFILE_TILE")) {
+  if (GROUP != kDenGroupC || options().profile != "tile") {
     kern<<<grid, GROUP * IPC, per_item * IPC, st>>>(a, Fmax, g->max_tiles,
                                                     pad4(std::max(4, g->max_xpad)));
     return check_cuda(cudaGetLastError(), "fb_tile_kernel launch");
@@ -729,10 +730,9 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     const bool many = a.B >= 8 * 148;
     // Utterances fewer than SMs: more threads per numerator shorten its
     // per-frame latency chain (it runs next to the denominator pass).
-    const char *ng = std::getenv("LFMMI_NUM_GROUP");
     // 4 warps per numerator at every batch size: sweep (B = 1024) num pass
     // 7.8 ms vs 16.0 ms with one warp per utterance.
-    const int want = ng ? std::atoi(ng) : 128;
+    const int want = options().num_group;
     if (want == 128 && per_s <= size_t(kMaxSmem))
       return launch_tile_impl<Real, 128, 1, true>(a, g, per_s, st);
     if (want == 64 && per_s <= size_t(kMaxSmem))
@@ -759,16 +759,16 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     size_t per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad, a.T_pad,
                               pad4(a.rep_r * a.r_stride), a.rep_e * a.e_stride, real, 2, true)
                       .total;
-    if (per2 > size_t(kMaxSmem) || std::getenv("LFMMI_GLOBAL_SCALES")) {
+    if (per2 > size_t(kMaxSmem)) {
       b.sc_smem = 0;
       per2 = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad, a.T_pad,
                          pad4(a.rep_r * a.r_stride), a.rep_e * a.e_stride, real, 2, false)
                  .total;
     }
-    if (std::getenv("LFMMI_DEBUG"))
+    if (options().debug)
       std::fprintf(stderr, "[lfmmi] den tile smem single=%zu double=%zu limit=%d\n", per, per2,
                    kMaxSmem);
-    if (!a.leak_pi && per2 <= size_t(kMaxSmem) && !std::getenv("LFMMI_TILE_SINGLE_X")) {
+    if (!a.leak_pi && per2 <= size_t(kMaxSmem) && options().tile_xdb) {
       note_den_kernel("fb_tile_kernel<float,512,1,1,0,1> (XDB)");
       return launch_tile_impl2<float, kDenGroup, 1, true, false, true>(b, g, per2, st);
     }

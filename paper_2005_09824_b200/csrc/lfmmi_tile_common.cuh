@@ -1,4 +1,4 @@
-// Shared-memory helpers of the tile kernels (fb_tile_kernel, fb_chain_kernel):
+// Shared-memory helpers of the tile kernels (fb_tile_kernel, fb_split_kernel):
 // explicitly scheduled fp32 arc loops over byte-offset slot words.
 #pragma once
 

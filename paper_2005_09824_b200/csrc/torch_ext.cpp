@@ -91,10 +91,50 @@ int64_t graphs_create(int64_t num_pdfs, torch::Tensor row_num_states, torch::Ten
   return reinterpret_cast<int64_t>(g);
 }
 
+// Linear-chain batch over caller-owned device tensors (lfmmi_graphs_create_linear):
+// `items` (rows, 4) int32, `states` (sum S, 4) int32 (bit patterns).  The
+// Python owner keeps both tensors alive as long as the handle.
+int64_t graphs_create_linear(int64_t max_states, int64_t num_pdfs, torch::Tensor items,
+                             torch::Tensor states) {
+  need_cuda(items, torch::kInt32, "items");
+  need_cuda(states, torch::kInt32, "states");
+  TORCH_CHECK(items.dim() == 2 && items.size(1) == 4, "items must be (rows, 4)");
+  TORCH_CHECK(states.dim() == 2 && states.size(1) == 4, "states must be (sum S, 4)");
+  lfmmi_graphs *g = nullptr;
+  check(lfmmi_graphs_create_linear(int32_t(items.size(0)), int32_t(max_states), int32_t(num_pdfs),
+                                   items.data_ptr<int32_t>(),
+                                   reinterpret_cast<const uint32_t *>(states.data_ptr<int32_t>()), &g),
+        "lfmmi_graphs_create_linear");
+  return reinterpret_cast<int64_t>(g);
+}
+
+void set_option(const std::string &name, const std::string &value) {
+  check(lfmmi_set_option(name.c_str(), value.c_str()), "lfmmi_set_option");
+}
+
+std::string get_option(const std::string &name) {
+  char buf[256];
+  check(lfmmi_get_option(name.c_str(), buf, sizeof(buf)), "lfmmi_get_option");
+  return buf;
+}
+
+void reset_options() { lfmmi_reset_options(); }
+
 void graphs_destroy(int64_t h) { check(lfmmi_graphs_destroy(as_graphs(h)), "lfmmi_graphs_destroy"); }
 
 int64_t workspace_size(int64_t max_states, int64_t total_frames, int64_t precision) {
   return int64_t(lfmmi_workspace_size(int32_t(max_states), total_frames, int32_t(precision)));
+}
+
+// Every per-item array must hold exactly B entries: a numerator list or a
+// lengths vector of the wrong size would otherwise index past its end on the
+// device.  (Lengths outside [1, T_max] are caught on the device: item_frames.)
+void check_batch_sizes(int64_t B, const torch::Tensor &lengths,
+                       std::initializer_list<const torch::Tensor *> per_item) {
+  TORCH_CHECK(lengths.dim() == 1 && lengths.numel() == B, "lengths must have ", B,
+              " entries, got ", lengths.numel());
+  for (const torch::Tensor *t : per_item)
+    TORCH_CHECK(t->numel() == B, "per-item array has ", t->numel(), " entries, batch has ", B);
 }
 
 int64_t chain_loss_workspace_size(int64_t num_h, int64_t den_h, int64_t batch, int64_t max_frames,
@@ -122,6 +162,10 @@ void forward_backward(int64_t h, torch::Tensor row_map, torch::Tensor loglikes,
   need_cuda(fail_frames, torch::kInt32, "fail_frames");
   if (leak_pi.has_value() && leak_pi->defined()) need_cuda(*leak_pi, dt, "leak_pi");
   TORCH_CHECK(loglikes.dim() == 3, "loglikes must be (B, T, D)");
+  check_batch_sizes(loglikes.size(0), lengths, {&row_map});
+  TORCH_CHECK(posteriors.sizes() == loglikes.sizes(), "posteriors must match loglikes");
+  TORCH_CHECK(log_probs.numel() == loglikes.size(0) && fail_frames.numel() == loglikes.size(0),
+              "log_probs / fail_frames must have B entries");
   check(lfmmi_forward_backward(as_graphs(h), row_map.data_ptr<int64_t>(), int32_t(loglikes.size(0)),
                                int32_t(loglikes.size(1)), int32_t(loglikes.size(2)),
                                precision_of(loglikes), loglikes.data_ptr(),
@@ -154,6 +198,10 @@ void chain_loss(int64_t num_h, torch::Tensor num_row_map, int64_t den_h, torch::
   need_cuda(den_fail, torch::kInt32, "den_fail");
   need_cuda(totals, torch::kFloat64, "totals");
   TORCH_CHECK(loglikes.dim() == 3, "loglikes must be (B, T, D)");
+  TORCH_CHECK(grad.sizes() == loglikes.sizes(), "grad must match loglikes");
+  check_batch_sizes(loglikes.size(0), lengths, {&num_row_map, &den_row_map, &num_log_probs,
+                                                &den_log_probs, &num_fail, &den_fail});
+  TORCH_CHECK(totals.numel() >= 3, "totals must hold 3 doubles");
   check(lfmmi_chain_loss(as_graphs(num_h), num_row_map.data_ptr<int64_t>(), as_graphs(den_h),
                          den_row_map.data_ptr<int64_t>(), int32_t(loglikes.size(0)),
                          int32_t(loglikes.size(1)), int32_t(loglikes.size(2)),
@@ -185,6 +233,14 @@ void chain_loss_packed(int64_t num_h, torch::Tensor num_row_map, int64_t den_h,
   need_cuda(totals, torch::kFloat64, "totals");
   TORCH_CHECK(loglikes.dim() == 2, "packed loglikes must be (sum T, D)");
   TORCH_CHECK(grad.sizes() == loglikes.sizes(), "grad must match loglikes");
+  need_cuda(num_log_probs, torch::kFloat64, "num_log_probs");
+  need_cuda(den_log_probs, torch::kFloat64, "den_log_probs");
+  need_cuda(num_fail, torch::kInt32, "num_fail");
+  need_cuda(den_fail, torch::kInt32, "den_fail");
+  check_batch_sizes(lengths.size(0), lengths, {&num_row_map, &den_row_map, &num_log_probs,
+                                               &den_log_probs, &num_fail, &den_fail});
+  TORCH_CHECK(totals.numel() >= 3, "totals must hold 3 doubles");
+  TORCH_CHECK(total_frames == loglikes.size(0), "total_frames must equal the packed row count");
   check(lfmmi_chain_loss_packed(
             as_graphs(num_h), num_row_map.data_ptr<int64_t>(), as_graphs(den_h),
             den_row_map.data_ptr<int64_t>(), int32_t(lengths.size(0)), int32_t(max_frames),
@@ -262,6 +318,10 @@ std::string last_den_kernel() { return lfmmi_last_den_kernel(); }
 PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("graphs_create", &graphs_create);
   m.def("graphs_destroy", &graphs_destroy);
+  m.def("graphs_create_linear", &graphs_create_linear);
+  m.def("set_option", &set_option);
+  m.def("get_option", &get_option);
+  m.def("reset_options", &reset_options);
   m.def("workspace_size", &workspace_size);
   m.def("chain_loss_workspace_size", &chain_loss_workspace_size);
   m.def("forward_backward", &forward_backward);

@@ -115,12 +115,12 @@ def _check_compatible(batch, graphs) -> None:
 def _leak_distribution(graphs, opts: FBOptions, explicit_uniform: bool = False):
     """forward_backward.py:133-166.  Returns None for the default uniform
     distribution (the kernels synthesise 1/S_g) unless ``explicit_uniform``."""
+    custom = opts.leak_distribution
+    if custom is None and not explicit_uniform:
+        return None
     rows = graphs.final_probs.shape[0]
     s_max = graphs.max_states
-    custom = opts.leak_distribution
     if custom is None:
-        if not explicit_uniform:
-            return None
         pi = np.zeros((rows, s_max), dtype=np.float64)
         for r in range(rows):
             n = graphs.item_num_states[0] if graphs.is_broadcast else graphs.item_num_states[r]

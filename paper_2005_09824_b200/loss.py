@@ -16,6 +16,7 @@
 
 from __future__ import annotations
 
+import collections
 from dataclasses import dataclass
 
 import numpy as np
@@ -54,10 +55,12 @@ def chain_loss_device(values, lengths, numerators, denominator, opts: FBOptions 
     ext = _backend.require_cuda()
     dev = values.device
     B, T, D = values.shape
-    ng = device_graphs(numerators, dev)
-    dgr = device_graphs(denominator, dev)
+    _check_batch(numerators, B, "numerators")
+    _check_batch(denominator, B, "denominator")
     pn = _leak_distribution(numerators, opts)
     pd = _leak_distribution(denominator, opts)
+    ng = device_graphs(numerators, dev, linear_ok=values.dtype == torch.float32 and pn is None)
+    dgr = device_graphs(denominator, dev)
     pn = None if pn is None else torch.as_tensor(pn, dtype=values.dtype, device=dev)
     pd = None if pd is None else torch.as_tensor(pd, dtype=values.dtype, device=dev)
     if total_frames is None:
@@ -107,8 +110,13 @@ def chain_loss_packed(values, lengths, numerators, denominator, opts: FBOptions 
         total_frames = int(lens.sum()) if total_frames is None else total_frames
     if total_frames != N:
         raise ValueError(f"sum of lengths {total_frames} != packed rows {N}")
-    ng = device_graphs(_as_graph_batch(numerators, B), dev)
-    dgr = device_graphs(_as_graph_batch(denominator, B), dev)
+    denominator = _as_graph_batch(denominator, B)
+    _check_batch(numerators, B, "numerators")
+    _check_batch(denominator, B, "denominator")
+    # a list of numerator graphs goes straight to the per-utterance linear
+    # records (no padded ChainGraphBatch build)
+    ng = device_graphs(numerators, dev, linear_ok=values.dtype == torch.float32)
+    dgr = device_graphs(denominator, dev)
     if ng.num_pdfs != D or dgr.num_pdfs != D:
         raise ValueError(f"pdf dimension mismatch: values have {D}, graphs have "
                          f"{ng.num_pdfs}/{dgr.num_pdfs}")
@@ -153,6 +161,13 @@ def chain_loss(batch, numerators, denominator, opts: FBOptions = FBOptions(),
                            num_failed=num_failed)
 
 
+def _check_batch(graphs, batch_size, what):
+    """The device code indexes ``row_map[b]`` for every item: sizes must agree."""
+    n = len(graphs) if isinstance(graphs, (list, tuple)) else getattr(graphs, "batch_size", None)
+    if n is not None and int(n) != int(batch_size):
+        raise ValueError(f"{what} batch has {n} items, input has {batch_size}")
+
+
 # ------------------------------------------------------------------- torch API
 def _as_graph_batch(graphs, batch_size):
     if isinstance(graphs, (list, tuple)):
@@ -187,7 +202,10 @@ def _autograd_function():
                 x = x.float()
             lengths = input_lengths.to(device=x.device, dtype=torch.int32).contiguous()
             B = lengths.shape[0]
-            nums = _as_graph_batch(numerators, B)
+            # numerator lists stay lists (per-utterance linear records) unless a
+            # custom leak distribution needs the padded batch view
+            nums = (numerators if opts.leak_distribution is None and isinstance(numerators, (list, tuple))
+                    else _as_graph_batch(numerators, B))
             den = _as_graph_batch(denominator, B)
             if x.dim() == 2:  # ragged (sum T, D) input: device-side batching
                 grad, _, _, _, _, totals = chain_loss_packed(x, lengths, nums, den, opts)
@@ -197,7 +215,13 @@ def _autograd_function():
                 import torch.distributed as dist
 
                 dist.all_reduce(totals, op=dist.ReduceOp.SUM, group=process_group)
-            scale = (1.0 / totals[1]) if normalize_by_frames else totals.new_ones(())
+            if normalize_by_frames:
+                # every utterance failed => no frames: zero loss and gradient
+                # (not 0 * inf = NaN into the model), no host sync
+                frames = totals[1]
+                scale = torch.where(frames > 0, 1.0 / frames.clamp_min(1.0), frames.new_zeros(()))
+            else:
+                scale = totals.new_ones(())
             loss = -totals[0] * scale
             ctx.save_for_backward(grad, scale)
             ctx.in_dtype = input.dtype
@@ -244,16 +268,21 @@ class ChainLoss(_module_base()):
         self.opts = opts
         self.normalize_by_frames = normalize_by_frames
         self.process_group = process_group
-        self._den_cache = {}
+        self._den_cache = collections.OrderedDict()
 
     def _den_batch(self, batch_size):
         if hasattr(self.den_graph, "row_map"):
             return self.den_graph
-        if batch_size not in self._den_cache:
-            self._den_cache[batch_size] = ChainGraphBatch.broadcast(self.den_graph, batch_size)
-        return self._den_cache[batch_size]
+        den = self._den_cache.pop(batch_size, None)
+        if den is None:
+            den = ChainGraphBatch.broadcast(self.den_graph, batch_size)
+        self._den_cache[batch_size] = den  # most recent last; a few batch sizes at most
+        while len(self._den_cache) > 4:
+            self._den_cache.popitem(last=False)
+        return den
 
     def forward(self, input, input_lengths, num_graphs):
-        den = self._den_batch(input.shape[0])
+        # B = number of utterances (input may be ragged (sum T, D))
+        den = self._den_batch(int(input_lengths.shape[0]))
         return ChainFunction.apply(input, input_lengths, num_graphs, den, self.opts,
                                    self.normalize_by_frames, self.process_group)

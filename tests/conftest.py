@@ -22,3 +22,19 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+@pytest.fixture
+def lib_options():
+    """Set library dispatch options (lfmmi_set_option) for one test; every
+    option is reset to its default afterwards."""
+    from paper_2005_09824_b200 import _backend
+
+    e = _backend.ext()
+
+    def set_(**kw):
+        for k, v in kw.items():
+            e.set_option(k, str(v))
+
+    yield set_
+    e.reset_options()

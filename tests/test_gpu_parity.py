@@ -116,31 +116,32 @@ def test_three_phase_api(cuda, name):
 
 
 # ------------------------------------------------- BASELINE configs vs oracle
-def _kernel_env(kernel, monkeypatch):
-    """Denominator kernel selection shared by the parity tests."""
+def _kernel_env(kernel, lib_options):
+    """Kernel selection shared by the parity tests: denominator "tile" (one CTA
+    per utterance), "split1"/"split2" (2-CTA split, 1 or 2 clusters), "tile1x"
+    (tile kernel with one posterior slot buffer), "numtile" (numerators through
+    the generic tile kernel instead of the linear-chain kernel)."""
     if kernel == "tile":  # one CTA per utterance (no forward/backward split)
-        monkeypatch.setenv("LFMMI_SPLIT", "0")
+        lib_options(split=0)
     if kernel in ("split1", "split2"):  # 2-CTA split, several utterances per cluster
-        monkeypatch.setenv("LFMMI_SPLIT", "1")
-        monkeypatch.setenv("LFMMI_SPLIT_CLUSTERS", kernel[-1])
+        lib_options(split=1)
+        lib_options(split_clusters=kernel[-1])
+    if kernel == "tile1x":
+        lib_options(split=0, tile_xdb=0)
+    if kernel == "numtile":
+        lib_options(linear=0)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "fused", "fused1x",
+@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile",
                                     "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])
-def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
-    _kernel_env(kernel, monkeypatch)
-    if kernel == "tile1x":  # denominator tile kernel with a single posterior slot buffer
-        monkeypatch.setenv("LFMMI_TILE_SINGLE_X", "1")
-    if kernel in ("fused", "fused1x"):  # single-launch num+den+grad kernel (opt-in)
-        monkeypatch.setenv("LFMMI_FUSED", "1")
-    if kernel == "fused1x":  # ... with a single posterior slot buffer
-        monkeypatch.setenv("LFMMI_CHAIN_SINGLE_X", "1")
+def test_configs_vs_oracle(cuda, config, batch_size, kernel, lib_options):
+    _kernel_env(kernel, lib_options)
     if kernel == "group":  # force the generic group kernel for the denominator
-        monkeypatch.setenv("LFMMI_DISABLE_TILE", "1")
-        monkeypatch.setenv("LFMMI_DISABLE_STREAM", "1")
+        lib_options(tile=0)
+        lib_options(stream=0)
     w = synth.make_workload(config, seed=3, batch_size=batch_size)
     batch, nums, den = w.build(P)
     res = P.chain_loss(batch, nums, den)
@@ -151,17 +152,17 @@ def test_configs_vs_oracle(cuda, config, batch_size, kernel, monkeypatch):
 
 
 @pytest.mark.parametrize("kernel", ["stream", "stream1", "stream512", "group"])
-def test_large_graph_l2_path_vs_oracle(cuda, kernel, monkeypatch):
+def test_large_graph_l2_path_vs_oracle(cuda, kernel, lib_options):
     """Config 4 (20k states / 200k arcs / 2000 pdfs): the arc packs do not fit in
     shared memory.  "stream": coalesced 32-state tiles streamed from L2
     (fb_stream_kernel); "group": the generic CSR kernel with alpha read back
     from the HBM trellis."""
     if kernel == "group":
-        monkeypatch.setenv("LFMMI_DISABLE_STREAM", "1")
+        lib_options(stream=0)
     if kernel == "stream1":  # one CTA per utterance instead of a 2-CTA cluster
-        monkeypatch.setenv("LFMMI_STREAM_MODE", "1024x1")
+        lib_options(stream_mode="1024x1")
     if kernel == "stream512":  # 2-CTA clusters of 512 threads (two per SM when they fit)
-        monkeypatch.setenv("LFMMI_STREAM_MODE", "512x2")
+        lib_options(stream_mode="512x2")
     w = synth.make_workload("large", seed=3, batch_size=2)
     batch, nums, den = w.build(P)
     res = P.chain_loss(batch, nums, den)
@@ -250,21 +251,18 @@ def test_failure_semantics(cuda):
 @pytest.mark.parametrize("late", [False, True])
 @pytest.mark.parametrize("config,batch_size,kernel", [
     ("wsj_mono", 4, "auto"), ("wsj_mono", 4, "tile"), ("wsj_mono", 4, "split1"),
-    ("wsj_mono", 4, "tile1x"), ("wsj_mono", 4, "fused"),
+    ("wsj_mono", 4, "tile1x"), ("wsj_mono", 4, "numtile"),
     ("wsj_biphone", 3, "auto"), ("large", 2, "auto"), ("large", 2, "stream1")])
 def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kernel, late,
-                                                  monkeypatch):
+                                                  lib_options):
     """A NaN log-likelihood makes that utterance's column totals NaN -> it fails
     at that frame in both graphs (_kernels.py:114-118); the others are untouched
     and chain_loss excludes it (loss.py:61-69).  Covers the early-exit paths of
-    the XDB tile kernel, the fused kernel and the 1- and 2-CTA stream kernel."""
-    _kernel_env(kernel, monkeypatch)
-    if kernel == "tile1x":
-        monkeypatch.setenv("LFMMI_TILE_SINGLE_X", "1")
-    if kernel == "fused":
-        monkeypatch.setenv("LFMMI_FUSED", "1")
+    the XDB tile kernel, the linear and tile numerator kernels and the 1- and
+    2-CTA stream kernel."""
+    _kernel_env(kernel, lib_options)
     if kernel == "stream1":
-        monkeypatch.setenv("LFMMI_STREAM_MODE", "1024x1")
+        lib_options(stream_mode="1024x1")
     w = synth.make_workload(config, seed=9, batch_size=batch_size)
     batch, nums, den = w.build(P)  # make_batch rejects non-finite input: poison afterwards
     bad = 1
@@ -285,10 +283,10 @@ def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kern
 
 
 @pytest.mark.parametrize("mode", ["1024x1", "1024x2"])
-def test_stream_kernel_short_utterances(cuda, mode, monkeypatch):
+def test_stream_kernel_short_utterances(cuda, mode, lib_options):
     """1-, 2- and 3-frame utterances through the L2-streamed kernel (biphone-sized
     denominator): prologue / epilogue edges of the register row pipeline."""
-    monkeypatch.setenv("LFMMI_STREAM_MODE", mode)
+    lib_options(stream_mode=mode)
     w = synth.make_workload("wsj_biphone", seed=10, batch_size=4)
     rng = np.random.default_rng(0)
     seqs = [rng.normal(0, 2, (t, w.D)).astype(np.float32).astype(np.float64) for t in (1, 2, 3, 7)]
@@ -301,11 +299,11 @@ def test_stream_kernel_short_utterances(cuda, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("kernel", ["tile", "split1", "split2"])
-def test_split_kernel_short_and_odd_utterances(cuda, kernel, monkeypatch):
+def test_split_kernel_short_and_odd_utterances(cuda, kernel, lib_options):
     """1, 2, 3, 4, 7 and 300-frame utterances through the denominator tile kernels:
     midpoint h = T/2 at 0 (no backward posterior frames), odd T, and several
     utterances per cluster (split1: all in one cluster, pack bound once)."""
-    _kernel_env(kernel, monkeypatch)
+    _kernel_env(kernel, lib_options)
     w = synth.make_workload("wsj_mono", seed=10, batch_size=6)
     rng = np.random.default_rng(0)
     seqs = [rng.normal(0, 2, (t, w.D)).astype(np.float32).astype(np.float64)
@@ -319,10 +317,10 @@ def test_split_kernel_short_and_odd_utterances(cuda, kernel, monkeypatch):
 
 
 @pytest.mark.parametrize("kernel", ["tile", "split2"])
-def test_split_kernel_bitwise_batch_independent(cuda, kernel, monkeypatch):
+def test_split_kernel_bitwise_batch_independent(cuda, kernel, lib_options):
     """An utterance's result does not depend on its batch-mates or on which
     cluster / position in a cluster's list it lands (fixed reduction orders)."""
-    _kernel_env(kernel, monkeypatch)
+    _kernel_env(kernel, lib_options)
     w = synth.make_workload("wsj_mono", seed=11, batch_size=8)
     batch, nums, den = w.build(P)
     full = P.forward_backward(batch, den)
@@ -389,9 +387,9 @@ def test_pdf_mismatch_raises(cuda):
 
 
 @pytest.mark.parametrize("num_group", ["32", "64", "128"])
-def test_numerator_group_sizes(cuda, num_group, monkeypatch):
+def test_numerator_group_sizes(cuda, num_group, lib_options):
     """Numerator pass with 1, 2 or 4 warps per utterance (B < 2 x SMs default: 4)."""
-    monkeypatch.setenv("LFMMI_NUM_GROUP", num_group)
+    lib_options(linear=0, num_group=num_group)
     w = synth.make_workload("wsj_mono", seed=4, batch_size=6)
     batch, nums, den = w.build(P)
     res = P.chain_loss(batch, nums, den)
@@ -400,17 +398,15 @@ def test_numerator_group_sizes(cuda, num_group, monkeypatch):
     assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
 
 
-@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "fused", "stream"])
+@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "numtile", "stream"])
 @pytest.mark.parametrize("config,batch_size", [("wsj_mono", 7), ("sweep", 5),
                                                ("wsj_biphone", 3), ("large", 2)])
-def test_packed_ragged_batch_any_order(cuda, config, batch_size, kernel, monkeypatch):
+def test_packed_ragged_batch_any_order(cuda, config, batch_size, kernel, lib_options):
     """Device-side batching: (sum T, D) ragged input in caller (unsorted) order,
     no padding; grad comes back in the same ragged layout."""
     import torch
 
-    _kernel_env(kernel, monkeypatch)
-    if kernel == "fused":
-        monkeypatch.setenv("LFMMI_FUSED", "1")
+    _kernel_env(kernel, lib_options)
     if kernel == "stream" and config not in ("wsj_biphone", "large"):
         pytest.skip("stream kernel is for graphs beyond shared memory")
     w = synth.make_workload(config, seed=6, batch_size=batch_size)
@@ -436,13 +432,13 @@ def test_packed_ragged_batch_any_order(cuda, config, batch_size, kernel, monkeyp
 
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split1"])
-def test_zero_length_item_fails_alone(cuda, kernel, monkeypatch):
+def test_zero_length_item_fails_alone(cuda, kernel, lib_options):
     """The device APIs take lengths as a device tensor and do not read them back:
     a zero-length utterance is reported failed (NaN log-prob, failure frame 0)
     without touching memory, and the rest of the batch is unaffected."""
     import torch
 
-    _kernel_env(kernel, monkeypatch)
+    _kernel_env(kernel, lib_options)
     w = synth.make_workload("wsj_mono", seed=12, batch_size=4)
     batch, nums, den = w.build(P)
     ref = O.chain_loss(batch, nums, den, leak=1e-5)
