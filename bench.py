@@ -7,10 +7,15 @@
 One step = one LF-MMI loss + gradient over one synthetic batch of the named
 config (numerator pass + denominator pass, forward + backward + posteriors +
 grad), inputs resident in HBM, graphs uploaded once.  Between timed steps L2
-is flushed (a 512 MiB write, outside the timed events).  Multi-GPU: one
-process per GPU (torchrun), each rank runs its own batch (seed = rank) —
-weak scaling — and the three scalar totals are all-reduced over NCCL inside
-the step; time is the max over ranks.
+is flushed (a 512 MiB write, outside the timed events).
+
+Multi-GPU (one process per GPU, NCCL): ``--gpus N`` outside torchrun re-launches
+itself under ``torch.distributed.run`` (NCCL_DEBUG=INFO, so the communicator
+set-up is in the log).  ``--config sweep`` shards ONE global B=1024 batch over
+the ranks by LPT on T_b (I_den + I_num,b) (strong scaling, SURVEY.md §8(e));
+the other configs give every rank its own batch (seed = rank, weak scaling).
+The only collective is the all-reduce of the three scalar totals inside the
+step; time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -44,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
+    ap.add_argument("--no-extra-e2e", action="store_true",
+                    help="skip the numpy-API and fresh-numerator end-to-end legs")
     return ap.parse_args()
 
 
@@ -174,13 +181,214 @@ def cpu_reference_run(w, steps, warmup, sample_b=None):
                                  "B": len(w.seqs)}
 
 
+# ------------------------------------------------------------ multi-GPU plumbing
+def self_launch(args):
+    """``--gpus N`` outside torchrun: re-run this script as N ranks (one per
+    GPU) under torch.distributed.run on 127.0.0.1.  NCCL's INFO log goes to
+    per-process files; rank 0 summarises its communicator lines in the JSON."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", NCCL_LOG)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+NCCL_LOG = "/tmp/lfmmi_bench_nccl.%h.%p.log"
+
+
+def nccl_summary():
+    """Communicator lines of this process's NCCL INFO log (if it was enabled)."""
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    if not path:
+        return None
+    path = path.replace("%h", os.uname().nodename).replace("%p", str(os.getpid()))
+    try:
+        with open(path) as f:
+            lines = f.read().splitlines()
+    except OSError:
+        return {"log": "unreadable"}
+    keep = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines
+            if "NCCL INFO" in ln and any(k in ln for k in ("Init COMPLETE", "NVLS", "nvls",
+                                                           "Channel 00", "comm 0x", "P2P"))]
+    return {"lines": keep[:12], "nvls": any("NVLS" in k or "nvls" in k for k in keep)}
+
+
+def subset(w, idx):
+    idx = [int(i) for i in idx]
+    return type(w)(w.name, w.seed, w.S, w.I, w.D, np.asarray(w.lengths)[idx],
+                   [w.seqs[i] for i in idx], w.den, [w.num_phones[i] for i in idx])
+
+
+def rank_workload(args, rank, world):
+    """This rank's workload, the scaling mode and (strong scaling) shard info.
+
+    ``sweep`` (BASELINE config 5): ONE global batch (seed 0, B = 1024) split by
+    LPT on the estimated cost T_b (I_den + I_num,b) — every rank derives the
+    same assignment, no input scatter; work is fixed as N
+    grows (strong).  Other configs: a full batch per rank, seed = rank (weak).
+    """
+    from paper_2005_09824_b200 import parallel, synth
+
+    if args.config == "sweep":
+        g = synth.make_workload("sweep", seed=0, batch_size=args.batch)
+        costs = np.asarray(g.lengths) * (g.I + 2.0 * np.asarray([len(p) for p in g.num_phones]))
+        shards = parallel.lpt_shards(costs, world)
+        idx = shards[rank]
+        T_all = np.asarray(g.lengths)
+        per = [float(np.sum(costs[s])) for s in shards]
+        info = {"global_B": len(g.seqs), "global_frames": int(T_all.sum()),
+                "global_T_max": int(T_all.max()),
+                "shard_cost_imbalance": max(per) / (sum(per) / world),
+                "ideal_speedup_bound": ideal_bound(T_all, world)}
+        return subset(g, idx), "strong", info
+    return synth.make_workload(args.config, seed=rank, batch_size=args.batch), "weak", None
+
+
+def ideal_bound(lengths, G, sms=148, k=1):
+    """best speed-up on G GPUs over 1 when an
+    utterance's frames run one after another on one SM (k utterances per SM):
+    max(sum T / (148 k), T_max) / max(sum T / (G 148 k), T_max)."""
+    tot, tmax = float(np.sum(lengths)), float(np.max(lengths))
+    return max(tot / (sms * k), tmax) / max(tot / (G * sms * k), tmax)
+
+
+def config_keys(args, w, world, scaling, shard, extra):
+    """Identical ``config`` keys in both arms (the driver compares them)."""
+    cfg = {"workload": args.config, "seed": "rank" if scaling == "weak" else 0,
+           "B": int(len(w.seqs)) if shard is None else shard["global_B"],
+           "parallelism": f"dp{world} (sequence-sharded, scalar all-reduce)"}
+    if shard is not None:
+        cfg.update(shard)
+    cfg.update(extra)
+    return cfg
+
+
+# ------------------------------------------------------------ extra e2e legs
+def numpy_api_leg(P, batch, nums, den, args):
+    """End to end through the reference-compatible numpy API: ``chain_loss(batch,
+    numerators, denominator)`` with a host (B, T, D) f64 batch in and the f64
+    gradient back in host memory (what a caller of the reference gets)."""
+    import torch
+
+    steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        P.chain_loss(batch, nums, den)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = P.chain_loss(batch, nums, den)
+    dt = (time.perf_counter() - t0) / steps
+    B, T, D = batch.values.shape
+    frames = int(np.sum(batch.lengths))
+    del res
+    return {"value": frames / dt, "unit": "frames/s", "ms_per_step": dt * 1e3,
+            "h2d_bytes_per_step": int(B * T * D * 4 + B * 4),
+            "d2h_bytes_per_step": int(B * T * D * 8 + (3 + 2 * B) * 8),
+            "how": "P.chain_loss(LogLikBatch f64 numpy, ChainGraphBatch, ChainGraphBatch): "
+                   "host f64 -> pinned f32 (threaded) -> H2D, grad D2H as f64 into pinned "
+                   "memory returned as numpy; host wall clock, synchronous API"}
+
+
+def fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_local, e2e):
+    """Training-loop leg: every step draws a NEW set of numerator ChainGraph
+    objects (never used in a loss before, from a pool built up front as a data
+    loader would) and a new window of log-likelihoods from a pinned host pool;
+    the step assembles the numerator batch from per-utterance linear records
+    (no host scheduling, no cudaMalloc, one async H2D) and runs the loss."""
+    import torch
+
+    from paper_2005_09824_b200 import synth
+
+    B = len(w.seqs)
+    W = 3
+    # pool of fresh utterances: one window of B per step while the f64 draw stays
+    # under ~1 GB (WSJ-mono: 23 windows = every timed step new); cycled beyond
+    per_win = B * float(np.mean(w.lengths)) * w.D * 8
+    n_win = int(max(2, min(W + args.steps, 24, 1e9 // per_win)))
+    pool = synth.make_workload(w.name, seed=10_000 + w.seed if isinstance(w.seed, int) else 10_000,
+                               batch_size=B * n_win)
+    graphs = []
+    for ph in pool.num_phones:  # graph construction: data-loader work, outside the timing
+        arcs, n, fin = synth.numerator_arcs(ph, pool.D // 2)
+        graphs.append(P.ChainGraph(arcs, n, pool.D, 0, fin))
+    lens = np.asarray(pool.lengths, dtype=np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    host_L = torch.empty((int(offs[-1]), pool.D), dtype=torch.float32, pin_memory=True)
+    hl = host_L.numpy()
+    for b, x in enumerate(pool.seqs):
+        hl[offs[b]:offs[b + 1]] = x
+    host_len = torch.from_numpy(lens.astype(np.int32)).pin_memory()
+    win_rows = [int(offs[(j + 1) * B] - offs[j * B]) for j in range(n_win)]
+    # linear records + item table of each window (int32 x 4 per state / item)
+    win_rec = [16 * (B + sum(g.num_states for g in graphs[j * B:(j + 1) * B]))
+               for j in range(n_win)]
+    x_dev = [torch.empty((max(win_rows), pool.D), dtype=torch.float32, device=dev) for _ in range(2)]
+    l_dev = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(2)]
+    g_dev = torch.empty((max(win_rows), pool.D), dtype=torch.float32, device=dev)
+    opts = P.FBOptions()
+
+    def step(i):
+        j = i % n_win
+        r0, r1 = int(offs[j * B]), int(offs[(j + 1) * B])
+        x = x_dev[i & 1][: r1 - r0]
+        x.copy_(host_L[r0:r1], non_blocking=True)
+        ln = l_dev[i & 1]
+        ln.copy_(host_len[j * B:(j + 1) * B], non_blocking=True)
+        _, _, _, _, _, totals = P.chain_loss_packed(
+            x, ln, graphs[j * B:(j + 1) * B], den, opts,
+            max_frames=int(lens[j * B:(j + 1) * B].max()), total_frames=r1 - r0,
+            grad=g_dev[: r1 - r0])
+        if pg is not None:
+            torch.distributed.all_reduce(totals, group=pg)
+        return totals.to("cpu", non_blocking=True), r1 - r0
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    frames = 0
+    for i in range(W, W + args.steps):
+        _, n = step(i)
+        frames += n
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if pg is not None:
+        t = torch.tensor([ms, frames], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t[1:])
+        mx = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        ms, frames = float(mx.item()), int(t[1].item())
+    value = frames / (ms / 1e3)
+    out = {"value": value, "unit": "frames/s", "ms_per_step": ms / args.steps,
+           "fresh_graphs_per_step": B, "pool_utterances": B * n_win,
+           "reused": W + args.steps > n_win,
+           "h2d_bytes_per_step": int(np.mean(win_rows) * pool.D * 4 + B * 4 + np.mean(win_rec)),
+           "d2h_bytes_per_step": 24,
+           "how": "chain_loss_packed with a list of never-used ChainGraph numerators per step "
+                  "(per-utterance linear records concatenated into pinned memory, one async "
+                  "H2D) and a fresh window of log-likelihoods from a pinned pool"}
+    if e2e:
+        out["vs_resident_graph_e2e"] = value / e2e["value"]
+    return out
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from paper_2005_09824_b200 import synth
 
-    w = synth.make_workload(args.config, seed=0, batch_size=args.batch)
+    w, scaling, shard = rank_workload(args, 0, 1)
     steps = max(1, args.steps)
     # Bound the run: sample the batch so one step is ~<1.5 s of CPU work.
     sample = None
@@ -192,9 +400,9 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
         "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "B_sampled": info["B"], "frames": info["frames"],
-                   "seed": 0},
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_keys(args, w, world, scaling, shard,
+                              {"B_sampled": info["B"], "frames_sampled": info["frames"]}),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": info["cores"],
                          "kind": info["kind"],
                          "sample": f"{info['B']} sequences / {info['frames']} frames of "
@@ -224,7 +432,7 @@ def run_ours(args):
         pg = dist.group.WORLD
     ext = _backend.require_cuda()
 
-    w = synth.make_workload(args.config, seed=rank, batch_size=args.batch)
+    w, scaling, shard = rank_workload(args, rank, world)
     batch, nums, den = w.build(P)
     opts = P.FBOptions()
     B, T, D = batch.values.shape
@@ -279,21 +487,16 @@ def run_ours(args):
     clocks = sampler.stop() if sampler else None
     ms_per_step = total_ms / args.steps
     value = frames_all * args.steps / (total_ms / 1e3)
+    nccl = nccl_summary() if (pg is not None and rank == 0) else None
 
     # ---- dominant kernel timed alone (no collective), same inputs -----------
-    # Fused path (LFMMI_FUSED=1): the single chain launch.  Two-pass path
-    # (default): the denominator pass, the step's critical path (the numerator
-    # pass runs concurrently on an auxiliary stream; combine + totals ~10 us).
+    # The denominator pass is the step's critical path (the numerator pass runs
+    # concurrently on an auxiliary stream; combine + totals ~10 us).
     launches_per_step = int(ext.last_launch_count())
-    fused = launches_per_step == 1
 
     def dominant_launch():
-        if fused:
-            P.chain_loss_device(values, lengths, nums, den, opts, total_frames=frames_local,
-                                grad=grad)
-        else:
-            P.forward_backward_device(values, lengths, den, opts, posteriors=grad, mode=3,
-                                      total_frames=frames_local)
+        P.forward_backward_device(values, lengths, den, opts, posteriors=grad, mode=3,
+                                  total_frames=frames_local)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -312,8 +515,7 @@ def run_ours(args):
     A_step = algorithmic_bytes(batch.lengths, D, den_g.num_states, den_g.num_transitions, num_S,
                                num_I)
     # Denominator pass alone: no numerator graphs in its compulsory traffic.
-    A = A_step if fused else algorithmic_bytes(batch.lengths, D, den_g.num_states,
-                                               den_g.num_transitions, [0], [0])
+    A = algorithmic_bytes(batch.lengths, D, den_g.num_states, den_g.num_transitions, [0], [0])
     peaks = load_json(MEASURED_PEAKS) or {}
     peak = peaks.get("hbm_gbs")
     peak_src = "measured" if peak else "fallback"
@@ -323,7 +525,7 @@ def run_ours(args):
     # ncu traffic is recorded for the headline workload only (profiles/ncu_summary.json)
     traffic = None
     if ncu.get("workload", "wsj_mono") == args.config and args.batch is None:
-        traffic = ncu.get("chain_dram_bytes_per_launch" if fused else "den_dram_bytes_per_launch")
+        traffic = ncu.get("den_dram_bytes_per_launch")
 
     # ---- end-to-end through the public API with host buffers ----------------
     e2e = None
@@ -403,6 +605,12 @@ def run_ours(args):
                       "double-buffered) + D2H of the step's totals on a read-back stream; "
                       "grad stays on device"}
 
+    e2e_numpy = e2e_fresh = None
+    if not args.no_e2e and not args.no_extra_e2e and not args.profile:
+        e2e_numpy = numpy_api_leg(P, batch, nums, den, args)
+        e2e_fresh = fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_local,
+                                        e2e)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         fps, info = cpu_reference_run(w, 3, 1)
@@ -414,13 +622,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "fp32",
             "data": "synthetic",
-            "config": {"workload": args.config, "S_den": den_g.num_states,
-                       "I_den": den_g.num_transitions, "D": D, "B_per_gpu": B,
-                       "frames_per_gpu": frames_local, "T_max": T, "seed": "rank",
-                       "l2": "flushed (512 MiB write) before every timed step",
-                       "parallelism": f"dp{world} (sequence-sharded, scalar all-reduce)"},
+            "config": config_keys(args, w, world, scaling, shard,
+                                  {"S_den": den_g.num_states, "I_den": den_g.num_transitions,
+                                   "D": D, "B_per_gpu": B, "frames_per_gpu": frames_local,
+                                   "T_max": T,
+                                   "l2": "flushed (512 MiB write) before every timed step"}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": den_kernel,
@@ -428,8 +636,9 @@ def run_ours(args):
                          "algorithmic_bytes_per_step": A_step,
                          "peak_source": peak_src},
             "kernel_share_of_step": kernel_ms / ms_per_step,
-            "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "cpu_baseline": cpu,
-            "clocks": clocks,
+            "e2e": e2e, "e2e_numpy_api": e2e_numpy, "e2e_fresh_numerators": e2e_fresh,
+            "gpu_launches": launches_per_step * args.steps, "cpu_baseline": cpu,
+            "clocks": clocks, "nccl": nccl,
         }
         print(json.dumps(line), flush=True)
     if pg is not None:
@@ -438,6 +647,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

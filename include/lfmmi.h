@@ -78,6 +78,10 @@ int32_t lfmmi_last_launch_count(void);
  */
 const char *lfmmi_last_den_kernel(void);
 
+/* Name of the kernel of the last forward-backward launch of any graph size on
+ * this thread (numerator passes included, e.g. "fb_linear_kernel<4>"). */
+const char *lfmmi_last_kernel(void);
+
 /*
  * Build a device-resident graph batch from the reference's padded host
  * layout (graph.py:253-279).  G physical rows; row r has row_num_states[r]

@@ -481,9 +481,12 @@ extern "C" int32_t lfmmi_last_launch_count(void) { return g_launches; }
 
 namespace {
 thread_local const char *g_den_kernel = "";
+thread_local const char *g_kernel = "";
 }
-void lfmmi::note_den_kernel(const char *name) { g_den_kernel = name; }
+void lfmmi::note_kernel(const char *name) { g_kernel = name; }
+void lfmmi::note_den_kernel(const char *name) { g_den_kernel = g_kernel = name; }
 extern "C" const char *lfmmi_last_den_kernel(void) { return g_den_kernel; }
+extern "C" const char *lfmmi_last_kernel(void) { return g_kernel; }
 
 static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_row_map,
                                 const lfmmi_graphs *denominator, const int64_t *den_row_map,

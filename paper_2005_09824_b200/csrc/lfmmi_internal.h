@@ -106,4 +106,6 @@ int set_error(int code, const std::string &msg);
 int check_cuda(cudaError_t err, const char *what);
 // Records the kernel of the last denominator-sized launch (lfmmi_last_den_kernel).
 void note_den_kernel(const char *name);
+// Records the kernel of the last forward-backward launch of any size (lfmmi_last_kernel).
+void note_kernel(const char *name);
 }  // namespace lfmmi

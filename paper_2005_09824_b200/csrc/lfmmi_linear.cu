@@ -373,6 +373,10 @@ int launch_k(const FBArgs<float> &a, cudaStream_t st) {
                               "cudaFuncSetAttribute(linear)");
     if (rc) return rc;
   }
+  static const char *const names[] = {"fb_linear_kernel<1>", "fb_linear_kernel<2>", "",
+                                       "fb_linear_kernel<4>", "", "", "", "fb_linear_kernel<8>",
+                                       "", "", "", "", "", "", "", "fb_linear_kernel<16>"};
+  note_kernel(names[K - 1]);
   fb_linear_kernel<K><<<a.B, 32, smem, st>>>(a);
   return check_cuda(cudaGetLastError(), "fb_linear_kernel launch");
 }

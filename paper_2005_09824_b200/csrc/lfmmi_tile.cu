@@ -726,7 +726,7 @@ int launch_tile(const FBArgs<Real> &a, const lfmmi_graphs *g, bool warp_per_item
     // Several utterances per CTA, but keep at least ~one CTA per SM busy.
     const size_t per_s = tile_layout(true, Fmax, g->max_tiles, a.D, X_pad, a.S_pad, a.D_pad,
                                      a.T_pad, RB, EB, real).total;
-    note_den_kernel("fb_tile_kernel<Real,{128,64,32},*> (numerator-sized graphs)");
+    note_kernel("fb_tile_kernel<Real,{128,64,32},*> (numerator-sized graphs)");
     const bool many = a.B >= 8 * 148;
     // Utterances fewer than SMs: more threads per numerator shorten its
     // per-frame latency chain (it runs next to the denominator pass).

@@ -314,6 +314,7 @@ void posterior_kernel(int64_t h, torch::Tensor row_map, torch::Tensor expl, torc
 std::string version() { return lfmmi_version(); }
 int64_t last_launch_count() { return lfmmi_last_launch_count(); }
 std::string last_den_kernel() { return lfmmi_last_den_kernel(); }
+std::string last_kernel() { return lfmmi_last_kernel(); }
 
 PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("graphs_create", &graphs_create);
@@ -333,4 +334,5 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.def("version", &version);
   m.def("last_launch_count", &last_launch_count);
   m.def("last_den_kernel", &last_den_kernel);
+  m.def("last_kernel", &last_kernel);
 }

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _backend
 from .forward_backward import (FBOptions, _check_compatible, _dtype, _leak_distribution,
-                               _to_device, _workspace)
+                               _to_device, _to_host_f64, _workspace)
 from .graph import ChainGraphBatch, device_graphs
 
 __all__ = ["ChainLossResult", "chain_loss", "chain_loss_device", "chain_loss_packed",
@@ -143,21 +143,25 @@ def chain_loss(batch, numerators, denominator, opts: FBOptions = FBOptions(),
     _check_compatible(batch, denominator)
     _backend.require_cuda()
     dev, values, lengths = _to_device(batch, _dtype(precision))
+    import torch
+
     grad, num_lp, den_lp, num_fail, den_fail, totals = chain_loss_device(
         values, lengths, numerators, denominator, opts, total_frames=batch.total_frames)
-    tot = totals.cpu().numpy()
+    # one read-back: totals + per-utterance log-probs, then the gradient (f64,
+    # the reference's dtype) into pinned memory; a single synchronisation
+    small = torch.cat([totals, num_lp, den_lp]).to("cpu", non_blocking=True)
+    grad_h = _to_host_f64(grad)
+    torch.cuda.current_stream(dev).synchronize()
+    small = small.numpy()
+    tot, nl, dl = small[:3], small[3:3 + batch.batch_size], small[3 + batch.batch_size:]
     num_failed = int(round(tot[2]))
     if num_failed == batch.batch_size:
         raise RuntimeError(f"all {batch.batch_size} utterances failed numerically")
     objective = float(tot[0])
     frames = int(round(tot[1]))
     loss = -objective / frames if normalize_by_frames else -objective
-    nl, dl = num_lp.cpu().numpy(), den_lp.cpu().numpy()
     per_utt = [(float(nl[b]), float(dl[b])) for b in range(batch.batch_size)]
-    import torch
-
-    return ChainLossResult(objective=objective, loss=loss,
-                           grad=grad.to(torch.float64).cpu().numpy(), per_utt=per_utt,
+    return ChainLossResult(objective=objective, loss=loss, grad=grad_h.numpy(), per_utt=per_utt,
                            num_failed=num_failed)
 
 
