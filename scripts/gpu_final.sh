@@ -16,4 +16,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"fb_split_kernel" -s 2 -c 1 -o gpurun_out/prof_den python bench.py --profile --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_den.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"fb_tile_kernel<float, .int.128" -s 2 -c 1 -o gpurun_out/prof_num python bench.py --profile --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_num.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fb_stream_kernel" -s 1 -c 1 -o gpurun_out/prof_stream python bench.py --config large --profile --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_stream.log 2>&1
-LFMMI_SPLIT=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"fb_tile_kernel<float, .int.512" -s 2 -c 1 -o gpurun_out/prof_tile python bench.py --profile --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_tile.log 2>&1
+LFMMI_OPTIONS=split=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"fb_tile_kernel<float, .int.512" -s 2 -c 1 -o gpurun_out/prof_tile python bench.py --profile --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_tile.log 2>&1

@@ -30,6 +30,6 @@ step = lambda: P.chain_loss_device(v, l, nums, den, total_frames=tf, grad=g)
 for rep in range(2):
     for nc in ["62", "63", "64", "65", "66"]:
         for h in ["32", "33", "34"]:
-            os.environ["LFMMI_SPLIT_CLUSTERS"] = nc
-            os.environ["LFMMI_SPLIT_H64"] = h
+            P._backend.ext().set_option("split_clusters", nc)
+            P._backend.ext().set_option("split_h64", h)
             print("rep", rep, "clusters", nc, "h64", h, "step_ms", round(timeit(step), 4), flush=True)
