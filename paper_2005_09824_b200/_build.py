@@ -19,8 +19,13 @@ import sysconfig
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB_DIR = os.path.join(PKG, "_lib")
 INCLUDE = os.path.join(ROOT, "include")
+# Build-time variants for same-box A/B measurements (development only): an
+# extra set of -D flags, built into _lib_<name>/ and selected at import time
+# by LFMMI_LIB_VARIANT=<name>.  The default build is _lib/.
+VARIANTS = {"rows8": ["-DLFMMI_SLOT_ROWS=8"]}
+VARIANT = os.environ.get("LFMMI_LIB_VARIANT", "")
+LIB_DIR = os.path.join(PKG, "_lib" + (f"_{VARIANT}" if VARIANT else ""))
 CORE_SO = os.path.join(LIB_DIR, "libpaper_lfmmi.so")
 TORCH_SO = os.path.join(LIB_DIR, "_lfmmi_torch" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 
@@ -54,6 +59,7 @@ def build_core(verbose=True, force=False):
     objs = [os.path.join(LIB_DIR, os.path.basename(s) + ".o") for s in srcs]
     cmds = [[NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
              "-Xptxas", "-v" if os.environ.get("LFMMI_PTXAS_VERBOSE") else "-O3",
+             *VARIANTS.get(VARIANT, []),
              "-x", "cu" if s.endswith(".cu") else "c++",
              "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o] for s, o in zip(srcs, objs)]
     # translation units are independent: compile them concurrently

@@ -2,6 +2,8 @@
 // explicitly scheduled fp32 arc loops over byte-offset slot words.
 #pragma once
 
+#include <type_traits>
+
 #include "lfmmi_device.cuh"
 
 namespace lfmmi {
@@ -99,46 +101,68 @@ __device__ __forceinline__ void sts_f(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(a), "f"(v));
 }
 
+// Pairwise sum of N terms ((t0 + t1) + (t2 + t3) for N = 4: the order the
+// 4-row loops always used, so N = 4 builds are bit-identical to before).
+template <int N>
+__device__ __forceinline__ float pair_sum(const float *t) {
+  if constexpr (N == 1) {
+    return t[0];
+  } else {
+    return pair_sum<N / 2>(t) + pair_sum<N / 2>(t + N / 2);
+  }
+}
+
+// Slot rows per unrolled step of the arc loops below: every step issues all of
+// its slot-word loads, then all emission / column gathers, then the math, so a
+// warp keeps 3 x kSlotRows shared loads in flight (build-time: -DLFMMI_SLOT_ROWS).
+#ifndef LFMMI_SLOT_ROWS
+#define LFMMI_SLOT_ROWS 4
+#endif
+constexpr int kSlotRows = LFMMI_SLOT_ROWS;
+static_assert(kSlotRows == 4 || kSlotRows == 8, "slot rows per step: 4 or 8");
+
+// Runs body<N>(row offset) over `trips` slot rows: steps of kSlotRows, then the
+// remainder as at most one 4-, one 2- and one 1-row step (no remainder loop).
+template <typename F>
+__device__ __forceinline__ void slot_rows(int trips, F &&body) {
+  int j = 0;
+#pragma unroll 1
+  for (; j + kSlotRows <= trips; j += kSlotRows) body(j, std::integral_constant<int, kSlotRows>{});
+  if constexpr (kSlotRows > 4) {
+    if (j + 4 <= trips) {
+      body(j, std::integral_constant<int, 4>{});
+      j += 4;
+    }
+  }
+  if (j + 2 <= trips) {
+    body(j, std::integral_constant<int, 2>{});
+    j += 2;
+  }
+  if (j < trips) body(j, std::integral_constant<int, 1>{});
+}
+
 // Forward arc sums of one tile lane, fp32 (slots hold byte-offset words):
 // A = sum p e[pdf] r[src], Bs = sum p e[pdf] (leak mass, uniform pi).
 template <bool LEAKY>
 __device__ __forceinline__ void fwd_tile_f32(uint32_t sb, int trips, uint32_t e32, uint32_t r32,
                                              float &A, float &Bs) {
-  int j = 0;
-#pragma unroll 1
-  for (; j + 4 <= trips; j += 4, sb += 4 * 256) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
-                w3 = lds_v2(sb + 768);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
-                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
-    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu)),
-                r2 = lds_f(r32 + (w2.x & 0xFFFFu)), r3 = lds_f(r32 + (w3.x & 0xFFFFu));
-    const float q0 = __uint_as_float(w0.y) * e0, q1 = __uint_as_float(w1.y) * e1,
-                q2 = __uint_as_float(w2.y) * e2, q3 = __uint_as_float(w3.y) * e3;
-    A = fmaf(q0, r0, A);
-    A = fmaf(q1, r1, A);
-    A = fmaf(q2, r2, A);
-    A = fmaf(q3, r3, A);
-    if (LEAKY) Bs += (q0 + q1) + (q2 + q3);
-  }
-  // Remainder (trips % 4 rows) without a loop: at most one pair and one single.
-  if (j + 2 <= trips) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
-    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu));
-    const float q0 = __uint_as_float(w0.y) * e0, q1 = __uint_as_float(w1.y) * e1;
-    A = fmaf(q0, r0, A);
-    A = fmaf(q1, r1, A);
-    if (LEAKY) Bs += q0 + q1;
-    j += 2;
-    sb += 2 * 256;
-  }
-  if (j < trips) {
-    const uint2 w = lds_v2(sb);
-    const float q = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16));
-    A = fmaf(q, lds_f(r32 + (w.x & 0xFFFFu)), A);
-    if (LEAKY) Bs += q;
-  }
+  slot_rows(trips, [&](int j, auto n) {
+    constexpr int N = decltype(n)::value;
+    uint2 w[N];
+    float e[N], r[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = lds_v2(sb + uint32_t(j + i) * 256u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) e[i] = lds_f(e32 + (w[i].x >> 16));
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = lds_f(r32 + (w[i].x & 0xFFFFu));
+    float q[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) q[i] = __uint_as_float(w[i].y) * e[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) A = fmaf(q[i], r[i], A);
+    if (LEAKY) Bs += pair_sum<N>(q);
+  });
 }
 
 // Backward arc sums of one tile lane, fp32: term = p e[pdf] (b[dst] + ld);
@@ -146,49 +170,25 @@ __device__ __forceinline__ void fwd_tile_f32(uint32_t sb, int trips, uint32_t e3
 __device__ __forceinline__ float bwd_tile_f32(uint32_t sb, uint32_t xb, int trips, uint32_t e32,
                                               uint32_t b32, uint32_t x32, float ld, float as) {
   float A = 0.f;
-  int j = 0;
-#pragma unroll 1
-  for (; j + 4 <= trips; j += 4, sb += 4 * 256, xb += 4 * 64) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
-                w3 = lds_v2(sb + 768);
-    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64), x2 = lds_h(xb + 128),
-                   x3 = lds_h(xb + 192);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
-                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
-    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu)),
-                b2 = lds_f(b32 + (w2.x & 0xFFFFu)), b3 = lds_f(b32 + (w3.x & 0xFFFFu));
-    const float t0 = __uint_as_float(w0.y) * e0 * (b0 + ld),
-                t1 = __uint_as_float(w1.y) * e1 * (b1 + ld),
-                t2 = __uint_as_float(w2.y) * e2 * (b2 + ld),
-                t3 = __uint_as_float(w3.y) * e3 * (b3 + ld);
-    A += (t0 + t1) + (t2 + t3);
-    sts_f(x32 + 4 * x0, as * t0);
-    sts_f(x32 + 4 * x1, as * t1);
-    sts_f(x32 + 4 * x2, as * t2);
-    sts_f(x32 + 4 * x3, as * t3);
-  }
-  if (j + 2 <= trips) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
-    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
-    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu));
-    const float t0 = __uint_as_float(w0.y) * e0 * (b0 + ld),
-                t1 = __uint_as_float(w1.y) * e1 * (b1 + ld);
-    A += t0 + t1;
-    sts_f(x32 + 4 * x0, as * t0);
-    sts_f(x32 + 4 * x1, as * t1);
-    j += 2;
-    sb += 2 * 256;
-    xb += 2 * 64;
-  }
-  if (j < trips) {
-    const uint2 w = lds_v2(sb);
-    const uint32_t x = lds_h(xb);
-    const float t = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16)) *
-                    (lds_f(b32 + (w.x & 0xFFFFu)) + ld);
-    A += t;
-    sts_f(x32 + 4 * x, as * t);
-  }
+  slot_rows(trips, [&](int j, auto n) {
+    constexpr int N = decltype(n)::value;
+    uint2 w[N];
+    uint32_t x[N];
+    float e[N], bb[N], t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = lds_v2(sb + uint32_t(j + i) * 256u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = lds_h(xb + uint32_t(j + i) * 64u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) e[i] = lds_f(e32 + (w[i].x >> 16));
+#pragma unroll
+    for (int i = 0; i < N; ++i) bb[i] = lds_f(b32 + (w[i].x & 0xFFFFu));
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = __uint_as_float(w[i].y) * e[i] * (bb[i] + ld);
+    A += pair_sum<N>(t);
+#pragma unroll
+    for (int i = 0; i < N; ++i) sts_f(x32 + 4 * x[i], as * t[i]);
+  });
   return A;
 }
 
@@ -199,49 +199,25 @@ __device__ __forceinline__ float fwd_post_tile_f32(uint32_t sb, uint32_t xb, int
                                                    uint32_t e32, uint32_t r32, uint32_t x32,
                                                    float lu, float cb) {
   float A = 0.f;
-  int j = 0;
-#pragma unroll 1
-  for (; j + 4 <= trips; j += 4, sb += 4 * 256, xb += 4 * 64) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
-                w3 = lds_v2(sb + 768);
-    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64), x2 = lds_h(xb + 128),
-                   x3 = lds_h(xb + 192);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
-                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
-    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu)),
-                r2 = lds_f(r32 + (w2.x & 0xFFFFu)), r3 = lds_f(r32 + (w3.x & 0xFFFFu));
-    const float t0 = __uint_as_float(w0.y) * e0 * (r0 + lu),
-                t1 = __uint_as_float(w1.y) * e1 * (r1 + lu),
-                t2 = __uint_as_float(w2.y) * e2 * (r2 + lu),
-                t3 = __uint_as_float(w3.y) * e3 * (r3 + lu);
-    A += (t0 + t1) + (t2 + t3);
-    sts_f(x32 + 4 * x0, cb * t0);
-    sts_f(x32 + 4 * x1, cb * t1);
-    sts_f(x32 + 4 * x2, cb * t2);
-    sts_f(x32 + 4 * x3, cb * t3);
-  }
-  if (j + 2 <= trips) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
-    const uint32_t x0 = lds_h(xb), x1 = lds_h(xb + 64);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
-    const float r0 = lds_f(r32 + (w0.x & 0xFFFFu)), r1 = lds_f(r32 + (w1.x & 0xFFFFu));
-    const float t0 = __uint_as_float(w0.y) * e0 * (r0 + lu),
-                t1 = __uint_as_float(w1.y) * e1 * (r1 + lu);
-    A += t0 + t1;
-    sts_f(x32 + 4 * x0, cb * t0);
-    sts_f(x32 + 4 * x1, cb * t1);
-    j += 2;
-    sb += 2 * 256;
-    xb += 2 * 64;
-  }
-  if (j < trips) {
-    const uint2 w = lds_v2(sb);
-    const uint32_t x = lds_h(xb);
-    const float t = __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16)) *
-                    (lds_f(r32 + (w.x & 0xFFFFu)) + lu);
-    A += t;
-    sts_f(x32 + 4 * x, cb * t);
-  }
+  slot_rows(trips, [&](int j, auto n) {
+    constexpr int N = decltype(n)::value;
+    uint2 w[N];
+    uint32_t x[N];
+    float e[N], r[N], t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = lds_v2(sb + uint32_t(j + i) * 256u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = lds_h(xb + uint32_t(j + i) * 64u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) e[i] = lds_f(e32 + (w[i].x >> 16));
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = lds_f(r32 + (w[i].x & 0xFFFFu));
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = __uint_as_float(w[i].y) * e[i] * (r[i] + lu);
+    A += pair_sum<N>(t);
+#pragma unroll
+    for (int i = 0; i < N; ++i) sts_f(x32 + 4 * x[i], cb * t[i]);
+  });
   return A;
 }
 
@@ -250,30 +226,20 @@ __device__ __forceinline__ float fwd_post_tile_f32(uint32_t sb, uint32_t xb, int
 __device__ __forceinline__ float bwd_plain_tile_f32(uint32_t sb, int trips, uint32_t e32,
                                                     uint32_t b32, float ld) {
   float A = 0.f;
-  int j = 0;
-#pragma unroll 1
-  for (; j + 4 <= trips; j += 4, sb += 4 * 256) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256), w2 = lds_v2(sb + 512),
-                w3 = lds_v2(sb + 768);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16)),
-                e2 = lds_f(e32 + (w2.x >> 16)), e3 = lds_f(e32 + (w3.x >> 16));
-    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu)),
-                b2 = lds_f(b32 + (w2.x & 0xFFFFu)), b3 = lds_f(b32 + (w3.x & 0xFFFFu));
-    A += (__uint_as_float(w0.y) * e0 * (b0 + ld) + __uint_as_float(w1.y) * e1 * (b1 + ld)) +
-         (__uint_as_float(w2.y) * e2 * (b2 + ld) + __uint_as_float(w3.y) * e3 * (b3 + ld));
-  }
-  if (j + 2 <= trips) {
-    const uint2 w0 = lds_v2(sb), w1 = lds_v2(sb + 256);
-    const float e0 = lds_f(e32 + (w0.x >> 16)), e1 = lds_f(e32 + (w1.x >> 16));
-    const float b0 = lds_f(b32 + (w0.x & 0xFFFFu)), b1 = lds_f(b32 + (w1.x & 0xFFFFu));
-    A += __uint_as_float(w0.y) * e0 * (b0 + ld) + __uint_as_float(w1.y) * e1 * (b1 + ld);
-    j += 2;
-    sb += 2 * 256;
-  }
-  if (j < trips) {
-    const uint2 w = lds_v2(sb);
-    A += __uint_as_float(w.y) * lds_f(e32 + (w.x >> 16)) * (lds_f(b32 + (w.x & 0xFFFFu)) + ld);
-  }
+  slot_rows(trips, [&](int j, auto n) {
+    constexpr int N = decltype(n)::value;
+    uint2 w[N];
+    float e[N], bb[N], t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = lds_v2(sb + uint32_t(j + i) * 256u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) e[i] = lds_f(e32 + (w[i].x >> 16));
+#pragma unroll
+    for (int i = 0; i < N; ++i) bb[i] = lds_f(b32 + (w[i].x & 0xFFFFu));
+#pragma unroll
+    for (int i = 0; i < N; ++i) t[i] = __uint_as_float(w[i].y) * e[i] * (bb[i] + ld);
+    A += pair_sum<N>(t);
+  });
   return A;
 }
 
