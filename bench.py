@@ -259,14 +259,16 @@ def ideal_bound(lengths, G, sms=148, k=1):
     return max(tot / (sms * k), tmax) / max(tot / (G * sms * k), tmax)
 
 
-def config_keys(args, w, world, scaling, shard, extra):
-    """Identical ``config`` keys in both arms (the driver compares them)."""
+def config_keys(args, w, world, scaling, shard):
+    """The ``config`` object, identical in both arms for the same command line
+    (the driver compares them); arm-specific details go to ``config_detail``."""
     cfg = {"workload": args.config, "seed": "rank" if scaling == "weak" else 0,
            "B": int(len(w.seqs)) if shard is None else shard["global_B"],
-           "parallelism": f"dp{world} (sequence-sharded, scalar all-reduce)"}
+           "parallelism": f"dp{world} (sequence-sharded, scalar all-reduce)",
+           "l2": "flushed (512 MiB write) before every timed step"}
     if shard is not None:
-        cfg.update(shard)
-    cfg.update(extra)
+        cfg["global_frames"] = shard["global_frames"]
+        cfg["global_T_max"] = shard["global_T_max"]
     return cfg
 
 
@@ -401,8 +403,8 @@ def run_reference_arm(args):
         "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_keys(args, w, world, scaling, shard,
-                              {"B_sampled": info["B"], "frames_sampled": info["frames"]}),
+        "config": config_keys(args, w, world, scaling, shard),
+        "config_detail": {"B_sampled": info["B"], "frames_sampled": info["frames"]},
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": info["cores"],
                          "kind": info["kind"],
                          "sample": f"{info['B']} sequences / {info['frames']} frames of "
@@ -624,11 +626,10 @@ def run_ours(args):
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "fp32",
             "data": "synthetic",
-            "config": config_keys(args, w, world, scaling, shard,
-                                  {"S_den": den_g.num_states, "I_den": den_g.num_transitions,
-                                   "D": D, "B_per_gpu": B, "frames_per_gpu": frames_local,
-                                   "T_max": T,
-                                   "l2": "flushed (512 MiB write) before every timed step"}),
+            "config": config_keys(args, w, world, scaling, shard),
+            "config_detail": {"S_den": den_g.num_states, "I_den": den_g.num_transitions,
+                              "D": D, "B_per_gpu": B, "frames_per_gpu": frames_local,
+                              "T_max": T, **(shard or {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": den_kernel,
