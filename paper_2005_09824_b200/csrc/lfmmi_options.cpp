@@ -25,6 +25,7 @@ const Field kFields[] = {
     {"split_clusters", &Options::split_clusters, nullptr},
     {"split_h64", &Options::split_h64, nullptr},
     {"stream_mode", nullptr, &Options::stream_mode},
+    {"stream_ring", &Options::stream_ring, nullptr},
     {"num_group", &Options::num_group, nullptr},
     {"tile_xdb", &Options::tile_xdb, nullptr},
     {"serial", &Options::serial, nullptr},

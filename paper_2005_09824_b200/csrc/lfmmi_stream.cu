@@ -46,13 +46,17 @@ namespace {
 constexpr int kStreamThreads = 1024;
 constexpr int kMaxD = 2048;  // log-likelihood row held in registers: kMaxD / NT per thread
 constexpr float kPostScale = 268435456.f;  // 2^28: posterior bins in uint32 fixed point
+constexpr int kRingRows = 4;               // slot rows per TMA chunk (4 x 256 B)
 
 struct StreamLayout {
-  unsigned vec, ebuf, bins, scales, shifts, part, mpart, total;
+  unsigned vec, ebuf, bins, scales, shifts, part, mpart, ring, bars, total;
+  int nslot;  // TMA ring slots per warp (0: slot rows read straight from L2)
 };
 
-__host__ __device__ inline StreamLayout stream_layout(int S32, int D_pad, int T_pad) {
+__host__ __device__ inline StreamLayout stream_layout(int S32, int D_pad, int T_pad, int NW = 0,
+                                                      int nslot = 0) {
   StreamLayout l;
+  l.nslot = nslot;
   unsigned o = 512;  // scratch: 32 doubles + 32 int64
   auto take = [&](unsigned bytes) {
     const unsigned at = o;
@@ -66,6 +70,8 @@ __host__ __device__ inline StreamLayout stream_layout(int S32, int D_pad, int T_
   l.shifts = take(unsigned(T_pad) * 4u);
   l.part = take(2u * 64u * 4u);
   l.mpart = take(2u * 32u * 4u);
+  l.ring = take(unsigned(NW) * unsigned(nslot) * kRingRows * 256u);
+  l.bars = take(unsigned(NW) * unsigned(nslot) * 8u);
   l.total = o;
   return l;
 }
@@ -80,7 +86,7 @@ __device__ __forceinline__ uint2 ldg_slot(const uint2 *p) {
 
 }  // namespace
 
-template <int NT, int CL>
+template <int NT, int CL, bool RING>
 __global__ void __launch_bounds__(NT, 1024 / NT)
     fb_stream_kernel(const FBArgs<float> a, int S32, const StreamLayout lay) {
   constexpr int NW = NT / 32;
@@ -209,8 +215,86 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     my_base = lane < ntw ? __ldg(base_arr + tl) : 0;
   };
 
+  // ---- TMA slot ring (RING) ---------------------------------------------------------
+  // Every frame re-reads the same slot rows, so each warp streams its tiles' rows
+  // into a private ring of nslot chunks (kRingRows x 256 B, cp.async.bulk
+  // completing on one mbarrier per slot) that runs nslot chunks ahead of the
+  // arc loop — across tile and frame boundaries — instead of a dependent L2
+  // load per row.  Counters are absolute (never reset), so slot = g % nslot
+  // and the wait parity is (g / nslot) & 1 across both phases.
+  uint2 *ring = reinterpret_cast<uint2 *>(smem + lay.ring);
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
+  const int nslot = lay.nslot;
+  unsigned g_cons = 0, g_iss = 0, g_end = 0;  // chunks consumed / issued / phase end
+  int p_i = 0, p_j = 0;                       // producer cursor: tile of this warp, row
+  const uint2 *pack = nullptr;
+  auto slot_ptr = [&](unsigned g) { return ring + (size_t(warp) * nslot + g % nslot) * (kRingRows * 32); };
+  auto slot_bar = [&](unsigned g) { return bars + warp * nslot + g % nslot; };
+  auto issue = [&]() {  // warp-converged: next chunk of the cursor into its slot
+    int trips = __shfl_sync(kFull, my_trips, p_i);
+    while (p_j >= trips) {  // skip empty tiles (wrapping to the next frame)
+      p_j = 0;
+      if (++p_i == ntw) p_i = 0;
+      trips = __shfl_sync(kFull, my_trips, p_i);
+    }
+    const int base = __shfl_sync(kFull, my_base, p_i);
+    const int n = min(kRingRows, trips - p_j);
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      bulk_copy_g2s(slot_ptr(g_iss), pack + base + 32 * p_j, unsigned(n) * 256u, slot_bar(g_iss));
+    }
+    ++g_iss;
+    p_j += kRingRows;
+  };
+  auto begin_phase = [&](const uint2 *pk, int frames) {
+    if constexpr (RING) {
+      pack = pk;
+      p_i = 0;
+      p_j = 0;
+      int c = 0;
+      for (int i = 0; i < ntw; ++i) c += (__shfl_sync(kFull, my_trips, i) + kRingRows - 1) / kRingRows;
+      g_end = g_iss + unsigned(c) * unsigned(frames);
+      for (int q = 0; q < nslot && g_iss < g_end; ++q) issue();
+    }
+  };
+  auto drain = [&]() {  // wait for copies still in flight (early exit of a phase)
+    if constexpr (RING) {
+      for (; g_cons < g_iss; ++g_cons) mbar_wait(slot_bar(g_cons), (g_cons / nslot) & 1u);
+      __syncwarp();
+    }
+  };
+  // Arc rows [0, trips) of one tile: body(w) per slot word (this lane's arc).
+  auto tile_rows = [&](const uint2 *sp, int trips, auto &&body) {
+    if constexpr (RING) {
+      for (int j0 = 0; j0 < trips; j0 += kRingRows) {
+        mbar_wait(slot_bar(g_cons), (g_cons / nslot) & 1u);
+        const uint2 *sl = slot_ptr(g_cons) + lane;
+        const int n = min(kRingRows, trips - j0);
+        uint2 w[kRingRows];
+#pragma unroll
+        for (int r = 0; r < kRingRows; ++r)
+          if (r < n) w[r] = sl[32 * r];
+        __syncwarp();  // every lane has its words: the slot may be refilled
+        ++g_cons;
+        if (g_iss < g_end) issue();
+#pragma unroll
+        for (int r = 0; r < kRingRows; ++r)
+          if (r < n) body(w[r]);
+      }
+    } else {
+#pragma unroll 8
+      for (int j = 0; j < trips; ++j) body(ldg_slot(sp + 32 * j));
+    }
+  };
+  if constexpr (RING) {
+    if (tid < NW * nslot) mbar_init(bars + tid, 1);
+    mbar_init_fence();
+    gsync();
+  }
+
   // ---- forward ---------------------------------------------------------------------
   load_meta(ftrips, fbase);
+  begin_phase(fwp, T);
   for (int s = tid; s < S32; s += NT) vec[s] = (s == init) ? 1.f : 0.f;
   {
     float r0[kEPT];
@@ -237,6 +321,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
       }
       if (!(t2 >= a.floor_eff) || isinf(t2)) {
         fail_at = k - 1;
+        drain();
         break;
       }
       inv2 = __frcp_rn(t2);
@@ -271,13 +356,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
         const int trips = __shfl_sync(kFull, my_trips, i);
         const uint2 *sp = fwp + __shfl_sync(kFull, my_base, i) + lane;
         float A = 0.f, Bs = 0.f;
-#pragma unroll 8
-        for (int j = 0; j < trips; ++j) {
-          const uint2 w = ldg_slot(sp + 32 * j);
+        tile_rows(sp, trips, [&](const uint2 w) {
           const float q = __uint_as_float(w.y) * e[w.x >> 15];
           A = fmaf(q, r[w.x & 0x7FFFu], A);
           Bs += q;
-        }
+        });
         if (s >= 0) {
           float raw = inv2 * (A + leakc * upi * Bs);
           if (last) raw *= fin[s];
@@ -338,6 +421,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
 
   // ---- backward + posteriors ------------------------------------------------------
   load_meta(btrips, bbase);
+  begin_phase(bwp, T);
   for (int d = tid; d < 2 * D_pad; d += NT) bins[d] = 0u;
   for (int s = tid; s < S32; s += NT) vec[(T & 1) * S32 + s] = s < S ? fin[s] * (1.f + lam) : 0.f;
   csync();  // peers' bins are zero before anyone accumulates
@@ -397,16 +481,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
         const int trips = __shfl_sync(kFull, my_trips, i);
         const uint2 *sp = bwp + __shfl_sync(kFull, my_base, i) + lane;
         float A = 0.f;
-#pragma unroll 8
-        for (int j = 0; j < trips; ++j) {
-          const uint2 w = ldg_slot(sp + 32 * j);
+        tile_rows(sp, trips, [&](const uint2 w) {
           const float pr = __uint_as_float(w.y);
           const unsigned pdf = w.x >> 15;
           const float term = pr * e[pdf] * (bt[w.x & 0x7FFFu] + ld);
           A += term;
           const unsigned q = __float2uint_rn(as * term * kPostScale);
           if (q) atomicAdd(bn + pdf, q);
-        }
+        });
         if (s >= 0) {
           const float v = inv * A;
           put2(bnew, bnew_p, s, v);
@@ -428,10 +510,16 @@ int launch_stream(const FBArgs<Real> &, const lfmmi_graphs *, cudaStream_t) {
   return set_error(LFMMI_ERR_UNSUPPORTED, "stream kernel is fp32-only");
 }
 
-template <int NT, int CL>
-static int launch_stream_impl(const FBArgs<float> &a, int S32, const StreamLayout &lay,
-                              cudaStream_t st) {
-  auto kern = fb_stream_kernel<NT, CL>;
+template <int NT, int CL, bool RING>
+static int launch_stream_impl2(const FBArgs<float> &a, int S32, const StreamLayout &lay,
+                               cudaStream_t st) {
+  auto kern = fb_stream_kernel<NT, CL, RING>;
+  note_den_kernel(NT == 1024 ? (CL == 2 ? (RING ? "fb_stream_kernel<1024,2> (TMA slot ring)"
+                                                : "fb_stream_kernel<1024,2>")
+                                        : (RING ? "fb_stream_kernel<1024,1> (TMA slot ring)"
+                                                : "fb_stream_kernel<1024,1>"))
+                             : (RING ? "fb_stream_kernel<512,2> (TMA slot ring)"
+                                     : "fb_stream_kernel<512,2>"));
   static bool configured = false;
   if (!configured) {
     int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -455,6 +543,21 @@ static int launch_stream_impl(const FBArgs<float> &a, int S32, const StreamLayou
   return check_cuda(cudaLaunchKernelEx(&cfg, kern, a, S32, lay), "fb_stream_kernel launch");
 }
 
+// TMA ring when it fits next to the columns (as many slots per warp as fit, up
+// to 4, at least 2), else slot rows straight from L2.
+template <int NT, int CL>
+static int launch_stream_impl(const FBArgs<float> &a, int S32, const StreamLayout &base,
+                              cudaStream_t st) {
+  constexpr int NW = NT / 32;
+  if (options().stream_ring) {
+    for (int ns = 4; ns >= 2; --ns) {
+      const StreamLayout lay = stream_layout(S32, a.D_pad, a.T_pad, NW, ns);
+      if (lay.total <= unsigned(kMaxSmem)) return launch_stream_impl2<NT, CL, true>(a, S32, lay, st);
+    }
+  }
+  return launch_stream_impl2<NT, CL, false>(a, S32, base, st);
+}
+
 template <>
 int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st) {
   if (!g->streamable) return set_error(LFMMI_ERR_UNSUPPORTED, "graph has no stream pack");
@@ -475,9 +578,6 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
   const std::string &want = options().stream_mode;  // "1024x1", "1024x2", "512x2"
   std::string mode = want != "auto" ? want : (2 * a.B <= sms ? "1024x2" : "1024x1");
-  note_den_kernel(mode == "1024x2"  ? "fb_stream_kernel<1024,2>"
-                  : mode == "512x2" ? "fb_stream_kernel<512,2>"
-                                    : "fb_stream_kernel<1024,1>");
   if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, S32, lay, st);
   if (mode == "512x2") return launch_stream_impl<512, 2>(a, S32, lay, st);
   return launch_stream_impl<1024, 1>(a, S32, lay, st);
