@@ -320,10 +320,67 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           for (int l = 0; l < 32; ++l) info.push_back(-1);
         }
       };
-      pack(iptr, &h.in_src[a0], &h.in_pdf[a0], &h.in_p64[a0], h.sf_info, h.sf_trips, h.sf_base,
-           h.sf_wp);
-      pack(optr, &h.out_dst[a0], &h.out_pdf[a0], &h.out_p64[a0], h.sb_info, h.sb_trips, h.sb_base,
-           h.sb_wp);
+      // Bank-scheduled rows: the stream kernel gathers plain (unreplicated)
+      // columns, so each row's arcs are chosen to spread the 32 lanes' column
+      // and emission addresses over the banks (greedy + a bounded local search:
+      // ~4M row evaluations per direction at most).
+      const GatherLayout plain{1, 0, 1, 0};
+      const int rows_est = std::max(1, I / 32 + nt);
+      const int iters = std::min(1500, int(4000000 / rows_est));
+      auto emit = [&](const TileSchedule &ts, const int *gidx, const int *pdf, const double *prob,
+                      std::vector<int> &info, std::vector<int> &trips, std::vector<int> &base,
+                      std::vector<uint2> &wp) {
+        int b = 0;
+        for (size_t t = 0; t < ts.trips.size(); ++t) {
+          for (int l = 0; l < 32; ++l) {
+            const unsigned v = ts.info[32 * t + l];
+            info.push_back((v & 0xFFFFu) == 0xFFFFu ? -1 : int(v & 0xFFFFu));
+          }
+          trips.push_back(ts.trips[t]);
+          base.push_back(b);
+          for (int j = 0; j < ts.trips[t]; ++j) {
+            // idle lanes re-read an address of an active lane (free broadcast), prob 0
+            const int *row = &ts.arc[size_t(ts.base[t]) + 32 * j];
+            unsigned pad = 0u;
+            for (int l = 0; l < 32; ++l)
+              if (row[l] >= 0) {
+                pad = unsigned(gidx[row[l]]) | (unsigned(pdf[row[l]]) << 15);
+                break;
+              }
+            for (int l = 0; l < 32; ++l) {
+              const int arc = row[l];
+              uint2 v{pad, 0u};
+              if (arc >= 0) {
+                const float f = float(prob[arc]);
+                v.x = unsigned(gidx[arc]) | (unsigned(pdf[arc]) << 15);
+                std::memcpy(&v.y, &f, 4);
+              }
+              wp.push_back(v);
+            }
+          }
+          b += 32 * ts.trips[t];
+        }
+        while (trips.size() % 4) {  // 16-byte aligned per-row tile arrays
+          trips.push_back(0);
+          base.push_back(0);
+          for (int l = 0; l < 32; ++l) info.push_back(-1);
+        }
+      };
+      if (S <= 0xFFFE) {  // schedule info packs states in 16 bits
+        const TileSchedule sf = schedule_tiles(S, iptr, &h.in_src[a0], &h.in_pdf[a0],
+                                               &h.in_p64[a0], plain, true, iters);
+        const TileSchedule sb = schedule_tiles(S, optr, &h.out_dst[a0], &h.out_pdf[a0],
+                                               &h.out_p64[a0], plain, true, iters);
+        emit(sf, &h.in_src[a0], &h.in_pdf[a0], &h.in_p64[a0], h.sf_info, h.sf_trips, h.sf_base,
+             h.sf_wp);
+        emit(sb, &h.out_dst[a0], &h.out_pdf[a0], &h.out_p64[a0], h.sb_info, h.sb_trips,
+             h.sb_base, h.sb_wp);
+      } else {
+        pack(iptr, &h.in_src[a0], &h.in_pdf[a0], &h.in_p64[a0], h.sf_info, h.sf_trips,
+             h.sf_base, h.sf_wp);
+        pack(optr, &h.out_dst[a0], &h.out_pdf[a0], &h.out_p64[a0], h.sb_info, h.sb_trips,
+             h.sb_base, h.sb_wp);
+      }
       d[kSTiles] = nt;
       max_stiles = std::max(max_stiles, nt);
     } else {

@@ -183,7 +183,9 @@ RowEval eval_row(const int *arcs, const int *gidx, const int *pdf, const GatherL
 }  // namespace
 
 TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
-                            const double *prob, const GatherLayout &gl, bool optimize) {
+                            const double *prob, const GatherLayout &gl, bool optimize,
+                            int iters_per_row) {
+  const int ls_iters = iters_per_row >= 0 ? iters_per_row : local_search_iters(S);
   std::vector<int> sorted(S);
   std::iota(sorted.begin(), sorted.end(), 0);
   std::stable_sort(sorted.begin(), sorted.end(), [&](int x, int y) {
@@ -322,7 +324,7 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
         }
       }
     }
-    if (optimize && trips > 1 && local_search_iters(S) > 0) {
+    if (optimize && trips > 1 && ls_iters > 0) {
       // slots[j][l] = CSR arc at row j, lane l (-1 idle); search over lane permutations.
       std::vector<std::array<int, 32>> slots(trips);
       for (int j = 0; j < trips; ++j)
@@ -330,7 +332,7 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
       std::vector<int> cost(trips);
       for (int j = 0; j < trips; ++j) cost[j] = eval_row(slots[j].data(), gidx, pdf, gl).cost;
       std::mt19937 rng(12345u + unsigned(w));
-      const int iters = local_search_iters(S) * trips;
+      const int iters = ls_iters * trips;
       for (int it = 0; it < iters; ++it) {
         const int l = int(rng() % 32u);
         const int j1 = int(rng() % unsigned(trips)), j2 = int(rng() % unsigned(trips));

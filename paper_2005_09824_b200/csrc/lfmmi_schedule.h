@@ -24,8 +24,10 @@ struct TileSchedule {
 };
 
 // ptr: CSR row pointers (S + 1) of the layout; gidx/pdf/prob per CSR arc.
+// iters_per_row < 0: the default local-search budget (option sched_iters / auto).
 TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
-                            const double *prob, const GatherLayout &gl, bool optimize);
+                            const double *prob, const GatherLayout &gl, bool optimize,
+                            int iters_per_row = -1);
 
 // Posterior slot of every backward tile slot: pdf groups (16-byte aligned,
 // `slack` spare positions each), conflict-avoiding positions per slot row,
