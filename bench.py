@@ -587,10 +587,14 @@ def run_ours(args):
 
         run(3)
         torch.cuda.synchronize()
-        flush.fill_(0)
-        torch.cuda.synchronize()
+        # L2 flush, then the timed region starts on the device right behind it:
+        # no host synchronisation in between, so the GPU never idles into a
+        # lower clock state before the first timed step (round-1 e2e carried a
+        # ~0.8 ms "first launch after idle" cost from exactly that gap)
         t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t_start.record(copy_stream)
+        flush.fill_(0)
+        t_start.record(stream)
+        copy_stream.wait_event(t_start)
         run(args.steps)
         t_end.record(d2h_stream)  # after the last step's totals reached the host buffer
         torch.cuda.synchronize()
