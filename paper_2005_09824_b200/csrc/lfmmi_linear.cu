@@ -54,12 +54,18 @@ __host__ __device__ inline LinLayout lin_layout(int T_max, int D, int K) {
   return l;
 }
 
+// K of one utterance: lanes own K states each, the smallest power of two with
+// 32 K >= S.  Chosen per utterance (not per batch), so an utterance's result
+// never depends on its batch-mates (bitwise batch independence).
+__device__ __forceinline__ int k_of(int S) {
+  return S <= 32 ? 1 : S <= 64 ? 2 : S <= 128 ? 4 : S <= 256 ? 8 : 16;
+}
+
 template <int K>
-__global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a) {
-  extern __shared__ __align__(16) float lsm[];
-  const int b = blockIdx.x, lane = threadIdx.x;
+__device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
+                                            const LinLayout &lay, int b) {
+  const int lane = threadIdx.x;
   const int D = a.D, T_max = a.T_max;
-  const LinLayout lay = lin_layout(T_max, D, K);
   float *scl = lsm;                    // per-frame scales (forward normalisers)
   float *shf = lsm + lay.T4;           // per-frame row maxima
   unsigned *hist = reinterpret_cast<unsigned *>(lsm + 2 * lay.T4);
@@ -362,22 +368,36 @@ __global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a) {
   cp_async_wait<0>();
 }
 
-template <int K>
-int launch_k(const FBArgs<float> &a, cudaStream_t st) {
-  const size_t smem = lin_layout(a.T_max, a.D, K).bytes;
-  if (smem > size_t(kMaxSmem)) return LFMMI_ERR_UNSUPPORTED;
+// One warp per utterance; this launch runs the utterances whose K lies in
+// [KLO, KHI] (the K = 16 variant needs ~2x the registers of the others, so it
+// is a separate launch that only batches with S > 256 pay for).  Shared-memory
+// strides follow the batch's largest K (`kstage`).
+template <int KLO, int KHI>
+__global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a, int kstage) {
+  extern __shared__ __align__(16) float lsm[];
+  const int b = blockIdx.x;
+  const int K = k_of(a.g.lin_item[a.row_map[b]].y);
+  if (K < KLO || K > KHI) return;
+  const LinLayout lay = lin_layout(a.T_max, a.D, kstage);
+  switch (K) {
+    case 1: if constexpr (KLO <= 1 && 1 <= KHI) linear_item<1>(a, lsm, lay, b); break;
+    case 2: if constexpr (KLO <= 2 && 2 <= KHI) linear_item<2>(a, lsm, lay, b); break;
+    case 4: if constexpr (KLO <= 4 && 4 <= KHI) linear_item<4>(a, lsm, lay, b); break;
+    case 8: if constexpr (KLO <= 8 && 8 <= KHI) linear_item<8>(a, lsm, lay, b); break;
+    default: if constexpr (KHI >= 16) linear_item<16>(a, lsm, lay, b); break;
+  }
+}
+
+template <int KLO, int KHI>
+int launch_range(const FBArgs<float> &a, int kstage, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
-    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_kernel<K>,
+    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_kernel<KLO, KHI>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    int(smem)),
                               "cudaFuncSetAttribute(linear)");
     if (rc) return rc;
   }
-  static const char *const names[] = {"fb_linear_kernel<1>", "fb_linear_kernel<2>", "",
-                                       "fb_linear_kernel<4>", "", "", "", "fb_linear_kernel<8>",
-                                       "", "", "", "", "", "", "", "fb_linear_kernel<16>"};
-  note_kernel(names[K - 1]);
-  fb_linear_kernel<K><<<a.B, 32, smem, st>>>(a);
+  fb_linear_kernel<KLO, KHI><<<a.B, 32, smem, st>>>(a, kstage);
   return check_cuda(cudaGetLastError(), "fb_linear_kernel launch");
 }
 
@@ -386,12 +406,14 @@ int launch_k(const FBArgs<float> &a, cudaStream_t st) {
 int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st) {
   if (!g->linear || a.leak_pi != nullptr || a.D > 65536) return LFMMI_ERR_UNSUPPORTED;
   const int S = g->max_states;
-  if (S <= 32) return launch_k<1>(a, st);
-  if (S <= 64) return launch_k<2>(a, st);
-  if (S <= 128) return launch_k<4>(a, st);
-  if (S <= 256) return launch_k<8>(a, st);
-  if (S <= 512) return launch_k<16>(a, st);
-  return LFMMI_ERR_UNSUPPORTED;
+  if (S > 512) return LFMMI_ERR_UNSUPPORTED;
+  const int kstage = S <= 32 ? 1 : S <= 64 ? 2 : S <= 128 ? 4 : S <= 256 ? 8 : 16;
+  const size_t smem = lin_layout(a.T_max, a.D, kstage).bytes;
+  if (smem > size_t(kMaxSmem)) return LFMMI_ERR_UNSUPPORTED;
+  note_kernel(kstage <= 8 ? "fb_linear_kernel<1..8>" : "fb_linear_kernel<1..8> + <16>");
+  const int rc = launch_range<1, 8>(a, kstage, smem, st);
+  if (rc || kstage <= 8) return rc;
+  return launch_range<16, 16>(a, kstage, smem, st);
 }
 
 }  // namespace lfmmi

@@ -30,6 +30,7 @@ __all__ = ["forward_kernel", "backward_kernel", "posterior_kernel", "install", "
 _LIB = None
 _HANDLES: dict = {}
 _SAVED: dict = {}
+CALLS = {"forward_kernel": 0, "backward_kernel": 0, "posterior_kernel": 0}  # seam traffic
 
 
 def library() -> ctypes.CDLL:
@@ -126,6 +127,7 @@ def forward_kernel(expl, lengths, bvalid, row_map, bw_from, bw_pdf, bw_prob, bw_
                    final_probs, init_states, leak, leak_pi, scale_floor, alpha, scales,
                    fail_frames):
     """``_kernels.forward_kernel`` (_kernels.py:54-122) on the GPU, in place."""
+    CALLS["forward_kernel"] += 1
     import torch
 
     B, T, D = expl.shape
@@ -168,6 +170,7 @@ def forward_kernel(expl, lengths, bvalid, row_map, bw_from, bw_pdf, bw_prob, bw_
 def backward_kernel(expl, lengths, bvalid, row_map, fw_to, fw_pdf, fw_prob, fw_index,
                     final_probs, scales, leak, leak_pi, fail_frames, beta):
     """``_kernels.backward_kernel`` (_kernels.py:125-191) on the GPU, in place."""
+    CALLS["backward_kernel"] += 1
     import torch
 
     B, T, D = expl.shape
@@ -197,6 +200,7 @@ def backward_kernel(expl, lengths, bvalid, row_map, fw_to, fw_pdf, fw_prob, fw_i
 def posterior_kernel(expl, lengths, row_map, item_ntrans, fw_from, fw_to, fw_pdf, fw_prob,
                      alpha, beta, fail_frames, gamma):
     """``_kernels.posterior_kernel`` (_kernels.py:194-224) on the GPU, in place."""
+    CALLS["posterior_kernel"] += 1
     import torch
 
     B, T, D = expl.shape

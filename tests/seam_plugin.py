@@ -17,6 +17,19 @@ def pytest_configure(config):
     config.lfmmi_seam = True
 
 
+def pytest_unconfigure(config):
+    """Record how many kernel calls went through the seam (the GPU kernels)."""
+    import json
+    import os
+
+    from paper_2005_09824_b200 import kernel_seam
+
+    path = os.environ.get("LFMMI_SEAM_REPORT")
+    if path:
+        with open(path, "w") as f:
+            json.dump(kernel_seam.CALLS, f)
+
+
 def pytest_report_header(config):
     import chainloss._kernels as k
 

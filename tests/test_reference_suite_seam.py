@@ -33,12 +33,18 @@ def test_reference_suite_through_gpu_seam(cuda, tmp_path):
     env["PYTHONPATH"] = os.pathsep.join([REF, SUITE, ROOT, os.path.join(ROOT, "tests")])
     env.setdefault("NUMBA_CACHE_DIR", str(tmp_path / "numba"))
     log = tmp_path / "suite.log"
+    report = tmp_path / "seam_calls.json"
+    env["LFMMI_SEAM_REPORT"] = str(report)
     cmd = [sys.executable, "-m", "pytest", SUITE, "-q", "-p", "seam_plugin", "-p",
            "no:cacheprovider", "-x", "--tb=short"]
     r = subprocess.run(cmd, env=env, cwd=str(tmp_path), capture_output=True, text=True,
                        timeout=1800)
     log.write_text(r.stdout + r.stderr)
     tail = "\n".join((r.stdout + r.stderr).splitlines()[-30:])
-    assert "lfmmi kernel seam" in r.stdout, tail
     assert r.returncode == 0, tail
     assert " passed" in r.stdout and " failed" not in r.stdout, tail
+    import json
+
+    calls = json.loads(report.read_text())  # the reference's kernels ran on the GPU
+    assert calls["forward_kernel"] > 100 and calls["backward_kernel"] > 50, calls
+    assert calls["posterior_kernel"] > 50, calls

@@ -29,7 +29,9 @@ def test_sanitizer_clean(cuda, tool, case):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not found")
     # this library's kernels only (fb_* and the combine kernel), not torch's
-    cmd = [SAN, "--tool", tool, "--error-exitcode", "97", "--kernel-name", "kns=fb_",
+    # (the stream kernel's TMA ring holds up to 128 mbarriers per CTA)
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "97", "--num-cuda-barriers", "256",
+           "--kernel-name", "kns=fb_",
            "--kernel-name", "kns=combine_kernel",
            sys.executable, os.path.join(ROOT, "scripts", "sanitize_case.py"), case]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
