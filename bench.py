@@ -446,6 +446,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        # communicator set-up lines into a per-process file (summarised in the JSON)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", NCCL_LOG)
         dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     ext = _backend.require_cuda()
