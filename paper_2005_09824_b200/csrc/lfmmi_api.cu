@@ -225,8 +225,10 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
               const void *L, const int *lengths, double leak, double floor, const void *leak_pi,
               void *work, size_t work_bytes, void *post, int mode, const int *other_fail,
               double *logp, int *fail, double *scale_logs, cudaStream_t st, bool packed,
-              int64_t total_frames) {
+              int64_t total_frames, const Real *E = nullptr, const Real *Em = nullptr) {
   FBArgs<Real> a{};
+  a.E = E;
+  a.Em = Em;
   a.g = graphs->dev;
   a.row_map = row_map;
   a.B = B;
@@ -335,7 +337,8 @@ static int forward_backward_impl(const lfmmi_graphs *graphs, const int64_t *row_
                                       size_t workspace_bytes, void *posteriors,
                                       int32_t post_mode, const int32_t *other_fail,
                                       double *log_probs, int32_t *fail_frames,
-                                      double *scale_logs, void *stream, bool packed) {
+                                      double *scale_logs, void *stream, bool packed,
+                                      const float *E = nullptr, const float *Em = nullptr) {
   int rc = check_common(graphs, batch, max_frames, num_pdfs, precision);
   if (rc) return rc;
   if (!row_map || !loglikes || !lengths || !workspace || !posteriors || !log_probs || !fail_frames)
@@ -357,7 +360,7 @@ static int forward_backward_impl(const lfmmi_graphs *graphs, const int64_t *row_
   return run_fused<float>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
                           scale_floor, leak_pi, workspace, workspace_bytes, posteriors, post_mode,
                           other_fail, log_probs, fail_frames, scale_logs, st, packed,
-                          total_frames);
+                          total_frames, E, Em);
 }
 
 
@@ -386,17 +389,22 @@ extern "C" int lfmmi_forward_backward_packed(LFMMI_FB_PARAMS) {
 static size_t chain_ws_parts(const lfmmi_graphs *num, const lfmmi_graphs *den, int32_t batch,
                              int32_t max_frames, int32_t num_pdfs, int64_t total_frames,
                              int32_t precision, size_t *den_off, size_t *num_off,
-                             size_t *gam_off) {
+                             size_t *gam_off, size_t *e_off = nullptr) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t es = precision == LFMMI_F64 ? 8 : 4;
   const size_t tf = size_t(std::max<int64_t>(total_frames, 1));
   const size_t den_b = al(lfmmi_workspace_size(den ? den->max_states : 1, int64_t(tf), precision));
   const size_t num_b = al(lfmmi_workspace_size(num ? num->max_states : 1, int64_t(tf), precision));
   const size_t gam_b = al(size_t(batch) * size_t(max_frames) * size_t(num_pdfs) * es);
+  // fp32: the step's emissions E = exp(L - m) + row maxima (emit_kernel), sized
+  // for the padded layout (>= the packed one)
+  const size_t rows = std::max(size_t(batch) * size_t(max_frames), tf);
+  const size_t e_b = precision == LFMMI_F32 ? al(rows * size_t(num_pdfs) * 4) + al(rows * 4) : 0;
   if (den_off) *den_off = 0;
   if (num_off) *num_off = den_b;
   if (gam_off) *gam_off = den_b + num_b;
-  return den_b + num_b + gam_b + 256;
+  if (e_off) *e_off = den_b + num_b + gam_b;
+  return den_b + num_b + gam_b + e_b + 256;
 }
 
 extern "C" size_t lfmmi_chain_loss_workspace_size(const lfmmi_graphs *numerators,
@@ -455,6 +463,54 @@ __global__ void combine_kernel(bool packed, int B, int T_max, int D, const int *
   }
 }
 
+// Emissions of one step (forward_backward.py:120-130): per valid row
+// m = max_d L (NaN-propagating) and E = exp(L - m), one warp per row.  The
+// passes that take E gather it instead of recomputing row maxima and exps
+// every frame of every recursion.
+__global__ void __launch_bounds__(256) emit_kernel(const float *__restrict__ L, const int *lengths,
+                                                   int T_max, int D, int packed, long long rows,
+                                                   float *__restrict__ E, float *__restrict__ Em) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += nw) {
+    if (!packed && int(r % T_max) >= item_frames(lengths, int(r / T_max), T_max)) continue;
+    const float *x = L + r * D;
+    float *e = E + r * D;
+    float m = -INFINITY;
+    if ((D & 3) == 0) {
+      const float4 *x4 = reinterpret_cast<const float4 *>(x);
+      for (int c = lane; c < (D >> 2); c += 32) {
+        const float4 v = x4[c];
+        m = nan_max(nan_max(m, v.x), nan_max(nan_max(v.y, v.z), v.w));
+      }
+      m = warp_max(m);
+      float4 *e4 = reinterpret_cast<float4 *>(e);
+      for (int c = lane; c < (D >> 2); c += 32) {
+        const float4 v = x4[c];
+        e4[c] = make_float4(expf(v.x - m), expf(v.y - m), expf(v.z - m), expf(v.w - m));
+      }
+    } else {
+      for (int d = lane; d < D; d += 32) m = nan_max(m, x[d]);
+      m = warp_max(m);
+      for (int d = lane; d < D; d += 32) e[d] = expf(x[d] - m);
+    }
+    if (lane == 0) Em[r] = m;
+  }
+}
+
+int lfmmi::launch_emit(const float *L, const int *lengths, int B, int T_max, int D, bool packed,
+                       int64_t rows, float *E, float *Em, cudaStream_t st) {
+  (void)B;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long want = (rows + 7) / 8;  // 8 rows (warps) per 256-thread block
+  const int grid = int(std::max<long long>(1, std::min<long long>(want, 8LL * sms)));
+  emit_kernel<<<grid, 256, 0, st>>>(L, lengths, T_max, D, packed ? 1 : 0, rows, E, Em);
+  return check_cuda(cudaGetLastError(), "emit_kernel launch");
+}
+
 namespace {
 thread_local int32_t g_launches = 0;
 struct AuxStream {
@@ -500,13 +556,15 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
                                 void *stream, bool packed) {
   if (!numerators || !denominator)
     return set_error(LFMMI_ERR_INVALID, "lfmmi_chain_loss: NULL graph handle");
-  size_t den_off, num_off, gam_off;
+  size_t den_off, num_off, gam_off, e_off;
   if (total_frames < 1 ||
       workspace_bytes < chain_ws_parts(numerators, denominator, batch, max_frames, num_pdfs,
-                                       total_frames, precision, &den_off, &num_off, &gam_off))
+                                       total_frames, precision, &den_off, &num_off, &gam_off,
+                                       &e_off))
     return set_error(LFMMI_ERR_INVALID, "workspace smaller than lfmmi_chain_loss_workspace_size");
   char *ws = static_cast<char *>(workspace);
   const size_t num_bytes = gam_off - num_off, den_bytes = num_off - den_off;
+  const float *E = nullptr, *Em = nullptr;
   auto st = static_cast<cudaStream_t>(stream);
   int rc = check_common(denominator, batch, max_frames, num_pdfs, precision);
   if (rc) return rc;
@@ -524,19 +582,31 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
   // per utterance) runs on the auxiliary stream next to the denominator pass
   // (one CTA per utterance).  The denominator is launched first so its CTAs
   // claim whole SMs; the numerator warps fill the SMs it leaves free.
+  // Emissions once per step, shared by the passes that take them (the linear
+  // numerator kernel and the split denominator kernel).
+  if (precision == LFMMI_F32 && options().emit) {
+    const size_t rows = packed ? size_t(total_frames) : size_t(batch) * size_t(max_frames);
+    float *e = reinterpret_cast<float *>(ws + e_off);
+    float *em = e + ((rows * size_t(num_pdfs) * 4 + 255) & ~size_t(255)) / 4;
+    rc = launch_emit(static_cast<const float *>(loglikes), lengths, batch, max_frames, num_pdfs,
+                     packed, int64_t(rows), e, em, st);
+    if (rc) return rc;
+    E = e;
+    Em = em;
+  }
   rc = check_cuda(cudaEventRecord(ax.fork, st), "cudaEventRecord(fork)");
   if (rc) return rc;
   rc = forward_backward_impl(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
                               loglikes, lengths, leak, scale_floor, den_leak_pi, total_frames,
                               ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE, nullptr, den_log_probs,
-                              den_fail, nullptr, stream, packed);
+                              den_fail, nullptr, stream, packed, E, Em);
   if (rc) return rc;
   rc = check_cuda(cudaStreamWaitEvent(ax.aux, ax.fork, 0), "cudaStreamWaitEvent(fork)");
   if (rc) return rc;
   rc = forward_backward_impl(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
                               loglikes, lengths, leak, scale_floor, num_leak_pi, total_frames,
                               ws + num_off, num_bytes, ws + gam_off, LFMMI_POST_WRITE, nullptr, num_log_probs,
-                              num_fail, nullptr, nst, packed);
+                              num_fail, nullptr, nst, packed, E, Em);
   if (rc) return rc;
   rc = check_cuda(cudaEventRecord(ax.join, nst), "cudaEventRecord(join)");
   if (rc) return rc;
@@ -560,7 +630,7 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
     rc = check_cuda(cudaGetLastError(), "combine_kernel launch");
     if (rc) return rc;
   }
-  g_launches = rc == LFMMI_OK ? 3 : 0;  // den, num, combine (+ totals)
+  g_launches = rc == LFMMI_OK ? (E ? 4 : 3) : 0;  // [emit,] den, num, combine (+ totals)
   return rc;
 }
 

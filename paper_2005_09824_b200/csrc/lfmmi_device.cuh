@@ -154,6 +154,10 @@ struct FBArgs {
   long long sc_total;  //   row maxima sc_total Reals further (ragged, like the trellis)
   int sc_smem;         //   ... or in shared memory (1; set by the launcher when they fit)
   long long *prof;     // split kernel debug timestamps (LFMMI_PROFILE_SPLIT), normally NULL
+  // Emissions computed once per step by emit_kernel (chain loss): E = exp(L - m)
+  // in L's layout and the row maxima m ((B, T_max) padded / (sum T) packed), or NULL.
+  const Real *E;
+  const Real *Em;
 };
 
 }  // namespace lfmmi

@@ -22,6 +22,7 @@
 
 #include "lfmmi_internal.h"
 #include "lfmmi_schedule.h"
+#include "lfmmi_options.h"
 
 namespace lfmmi {
 
@@ -427,7 +428,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           const int chore = std::min(kTableNW, (num_pdfs + 31) / 32);
           // (a frame's chores are latency chains — row max, exp, prefetch — worth
           // ~16 slot rows of arc work; measured: bias 2 -> 16, den 1.419 -> 1.294 ms)
-          constexpr int chore_bias = 16;
+          const int chore_bias = options().chore_bias;
           for (int w = kTableNW - chore; w < kTableNW; ++w) bias[w] = chore_bias;
           d[kWTabOff] = int(h.tf_wtab.size());
           warp_lists(tf.trips, bias, tab, lst);
@@ -439,7 +440,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
           int spl = 1;
           while (spl < 32 && num_pdfs * spl * 2 <= 32 * kTableNW) spl <<= 1;
           const int lanes = num_pdfs * spl;
-          constexpr int chore_bias_bwd = chore_bias;
+          const int chore_bias_bwd = chore_bias;
           for (int w = kTableNW - chore; w < kTableNW; ++w) bias[w] = chore_bias_bwd;
           if (lanes < 32 * kTableNW) {
             const int fw = (lanes + 31) / 32;

@@ -40,4 +40,8 @@ int launch_stream(const FBArgs<Real> &a, const lfmmi_graphs *graphs, cudaStream_
 // launching) when not applicable.
 int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st);
 
+// Emissions pre-pass (lfmmi_api.cu emit_kernel): E = exp(L - m), Em = m per valid row.
+int launch_emit(const float *L, const int *lengths, int B, int T_max, int D, bool packed,
+                int64_t rows, float *E, float *Em, cudaStream_t st);
+
 }  // namespace lfmmi

@@ -61,7 +61,10 @@ __device__ __forceinline__ int k_of(int S) {
   return S <= 32 ? 1 : S <= 64 ? 2 : S <= 128 ? 4 : S <= 256 ? 8 : 16;
 }
 
-template <int K>
+// PRE: the step's emissions E = exp(L - m) and row maxima come from emit_kernel
+// (chain loss), so a frame stages the E row and gathers it — no row maximum,
+// no exp; otherwise both are computed here from the staged L row.
+template <int K, bool PRE>
 __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
                                             const LinLayout &lay, int b) {
   const int lane = threadIdx.x;
@@ -79,7 +82,8 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
   off = warp_sum(off);
   const int T = item_frames(a.lengths, b, T_max);
   const size_t row0 = a.packed ? size_t(off) : size_t(b) * T_max;
-  const float *Lb = a.L + row0 * D;
+  const float *Lb = (PRE ? a.E : a.L) + row0 * D;
+  const float *Emb = PRE ? a.Em + (a.packed ? size_t(off) : size_t(b) * T_max) : nullptr;
   float *post_b = a.post + row0 * D;
   if (!reads_post && !a.packed)  // padded rows of this item
     for (size_t i = lane; i < size_t(T_max - T) * D; i += 32) post_b[size_t(T) * D + i] = 0.f;
@@ -121,7 +125,7 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
   const float leak = a.leak;
   const float vleak = leak > 0.f ? leak / (float(S) * (1.f + leak)) : 0.f;  // leak * pi / (1 + leak)
 
-  const bool vec16 = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.L) & 15) == 0);
+  const bool vec16 = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(Lb) & 15) == 0);
   auto stage = [&](int t) { return ring + (t % kRing) * lay.stage; };
   auto issue_row = [&](int t) {
     float *dst = stage(t);
@@ -144,7 +148,14 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
       for (int c = 0; c < K; ++c) cp_async_elem(dst + c, src + c);
     }
   };
-  auto emission = [&](const float *Lt, unsigned pdf, float m) { return expf(Lt[pdf] - m); };
+  auto emission = [&](const float *Lt, unsigned pdf, float m) {
+    if constexpr (PRE) {
+      (void)m;
+      return Lt[pdf];
+    } else {
+      return expf(Lt[pdf] - m);
+    }
+  };
 
   // ---- forward (_kernels.py:54-122) ---------------------------------------------
   float r[K];  // unnormalised column: alpha_0 (one-hot) at t = 0, raw_t after
@@ -170,10 +181,13 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
     // unnormalised stencil on column t
     float prev = __shfl_up_sync(kFull, r[K - 1], 1);
     if (lane == 0) prev = 0.f;
-    float m = -INFINITY;
-    for (int d = lane; d < D; d += 32) m = nan_max(m, Lt[d]);
+    float m = 0.f;
+    if constexpr (!PRE) {
+      m = -INFINITY;
+      for (int d = lane; d < D; d += 32) m = nan_max(m, Lt[d]);
+      m = warp_max(m);
+    }
     R = warp_sum(R);
-    m = warp_max(m);
     float A[K], Bv[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -196,7 +210,7 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
       u = rcp_rn(tot);
       if (lane == 0) scl[t - 1] = tot;
     }
-    if (lane == 0) shf[t] = m;
+    if (lane == 0) shf[t] = PRE ? Emb[t] : m;
     // normalised alpha_t -> trellis row t (posteriors of frame t in the backward)
     if (own_row) {
       float al[K];
@@ -237,10 +251,14 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
     // did not reach are still reported (forward_backward.py:184,206)
     for (int k = fail_at; k < T; ++k) {
       if (k > fail_at) {
-        float m = -INFINITY;
-        for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
-        m = warp_max(m);
-        if (lane == 0) shf[k] = m;
+        if constexpr (PRE) {
+          if (lane == 0) shf[k] = Emb[k];
+        } else {
+          float m = -INFINITY;
+          for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
+          m = warp_max(m);
+          if (lane == 0) shf[k] = m;
+        }
       }
       if (lane == 0) scl[k] = 1.f;
     }
@@ -372,7 +390,7 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
 // [KLO, KHI] (the K = 16 variant needs ~2x the registers of the others, so it
 // is a separate launch that only batches with S > 256 pay for).  Shared-memory
 // strides follow the batch's largest K (`kstage`).
-template <int KLO, int KHI>
+template <int KLO, int KHI, bool PRE>
 __global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a, int kstage) {
   extern __shared__ __align__(16) float lsm[];
   const int b = blockIdx.x;
@@ -380,24 +398,24 @@ __global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a, in
   if (K < KLO || K > KHI) return;
   const LinLayout lay = lin_layout(a.T_max, a.D, kstage);
   switch (K) {
-    case 1: if constexpr (KLO <= 1 && 1 <= KHI) linear_item<1>(a, lsm, lay, b); break;
-    case 2: if constexpr (KLO <= 2 && 2 <= KHI) linear_item<2>(a, lsm, lay, b); break;
-    case 4: if constexpr (KLO <= 4 && 4 <= KHI) linear_item<4>(a, lsm, lay, b); break;
-    case 8: if constexpr (KLO <= 8 && 8 <= KHI) linear_item<8>(a, lsm, lay, b); break;
-    default: if constexpr (KHI >= 16) linear_item<16>(a, lsm, lay, b); break;
+    case 1: if constexpr (KLO <= 1 && 1 <= KHI) linear_item<1, PRE>(a, lsm, lay, b); break;
+    case 2: if constexpr (KLO <= 2 && 2 <= KHI) linear_item<2, PRE>(a, lsm, lay, b); break;
+    case 4: if constexpr (KLO <= 4 && 4 <= KHI) linear_item<4, PRE>(a, lsm, lay, b); break;
+    case 8: if constexpr (KLO <= 8 && 8 <= KHI) linear_item<8, PRE>(a, lsm, lay, b); break;
+    default: if constexpr (KHI >= 16) linear_item<16, PRE>(a, lsm, lay, b); break;
   }
 }
 
-template <int KLO, int KHI>
+template <int KLO, int KHI, bool PRE>
 int launch_range(const FBArgs<float> &a, int kstage, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
-    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_kernel<KLO, KHI>,
+    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_kernel<KLO, KHI, PRE>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    int(smem)),
                               "cudaFuncSetAttribute(linear)");
     if (rc) return rc;
   }
-  fb_linear_kernel<KLO, KHI><<<a.B, 32, smem, st>>>(a, kstage);
+  fb_linear_kernel<KLO, KHI, PRE><<<a.B, 32, smem, st>>>(a, kstage);
   return check_cuda(cudaGetLastError(), "fb_linear_kernel launch");
 }
 
@@ -410,10 +428,16 @@ int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st
   const int kstage = S <= 32 ? 1 : S <= 64 ? 2 : S <= 128 ? 4 : S <= 256 ? 8 : 16;
   const size_t smem = lin_layout(a.T_max, a.D, kstage).bytes;
   if (smem > size_t(kMaxSmem)) return LFMMI_ERR_UNSUPPORTED;
-  note_kernel(kstage <= 8 ? "fb_linear_kernel<1..8>" : "fb_linear_kernel<1..8> + <16>");
-  const int rc = launch_range<1, 8>(a, kstage, smem, st);
+  const bool pre = a.E != nullptr;
+  note_kernel(kstage <= 8 ? (pre ? "fb_linear_kernel<1..8> (emissions pre-pass)"
+                                 : "fb_linear_kernel<1..8>")
+                          : (pre ? "fb_linear_kernel<1..8> + <16> (emissions pre-pass)"
+                                 : "fb_linear_kernel<1..8> + <16>"));
+  int rc = pre ? launch_range<1, 8, true>(a, kstage, smem, st)
+               : launch_range<1, 8, false>(a, kstage, smem, st);
   if (rc || kstage <= 8) return rc;
-  return launch_range<16, 16>(a, kstage, smem, st);
+  return pre ? launch_range<16, 16, true>(a, kstage, smem, st)
+             : launch_range<16, 16, false>(a, kstage, smem, st);
 }
 
 }  // namespace lfmmi

@@ -29,7 +29,9 @@ const Field kFields[] = {
     {"num_group", &Options::num_group, nullptr},
     {"tile_xdb", &Options::tile_xdb, nullptr},
     {"serial", &Options::serial, nullptr},
+    {"emit", &Options::emit, nullptr},
     {"sched_iters", &Options::sched_iters, nullptr},
+    {"chore_bias", &Options::chore_bias, nullptr},
     {"debug", &Options::debug, nullptr},
     {"profile", nullptr, &Options::profile},
 };

@@ -21,7 +21,9 @@ struct Options {
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
   int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots
   int serial = 0;         // chain_loss: numerator pass on the caller's stream
+  int emit = 1;           // chain_loss (fp32): emissions pre-pass shared by the passes
   int sched_iters = -1;   // bank-conflict local search moves per slot row (-1 auto)
+  int chore_bias = 16;    // den warp lists: extra slot rows charged to the chore warps (pack time)
   int debug = 0;          // layout / dispatch notes on stderr
   std::string profile;    // "" | "split" | "tile": per-frame cycle counters on stderr
 };

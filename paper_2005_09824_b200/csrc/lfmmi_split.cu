@@ -267,10 +267,15 @@ __global__ void __launch_bounds__(kNT, 1)
       scales = a.work + a.sc_off + item_off;
       shifts = scales + a.sc_total;
     }
-    const float *Lb = a.L + size_t(b) * a.T_max * D;
+    // With the emissions pre-pass (chain loss), the staged rows are E = exp(L - m)
+    // and the row maxima come precomputed: the chore warps only copy rows.
+    const bool pre = a.E != nullptr;
+    const float *Lb = (pre ? a.E : a.L) + size_t(b) * a.T_max * D;
+    const float *Emb = pre ? a.Em + size_t(b) * a.T_max : nullptr;
     float *post_b = a.post + size_t(b) * a.T_max * D;
     if (a.packed) {
-      Lb = a.L + size_t(item_off) * D;
+      Lb = (pre ? a.E : a.L) + size_t(item_off) * D;
+      if (pre) Emb = a.Em + size_t(item_off);
       post_b = a.post + size_t(item_off) * D;
     }
     // forward CTA: LPT lists without / with the flush chore (first / second half)
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kNT, 1)
       for (int d = ctid; d < D; d += kNT) cp_async_elem(dst + d, src + d);
     };
     auto row_max_part = [&](int t) {
-      if (t < 0 || t >= T || cwarp >= nrw) return;
+      if (pre || t < 0 || t >= T || cwarp >= nrw) return;
       const float *src = stage + (t & (kStageRing - 1)) * D_pad;
       float m = -INFINITY;
       for (int d = ctid; d < D; d += kNT) m = nan_max(m, src[d]);
@@ -294,11 +299,19 @@ __global__ void __launch_bounds__(kNT, 1)
     };
     auto compute_e = [&](int t, bool record_shift) {
       if (cwarp >= nrw) return;
+      const float *src = stage + (t & (kStageRing - 1)) * D_pad;
+      float *dst = ebuf + (t & 1) * EB;
+      if (pre) {  // staged row already holds exp(L - m)
+        for (int d = ctid; d < D; d += kNT) {
+          const float v = src[d];
+          for (int c = 0; c < a.rep_e; ++c) dst[c * a.e_stride + d] = v;
+        }
+        if (record_shift && ctid == 0) shifts[t] = Emb[t];
+        return;
+      }
       const float *mp = mpart + (t & 1) * 32;
       float m = lane < nrw ? mp[lane] : -INFINITY;
       m = warp_max(m);
-      const float *src = stage + (t & (kStageRing - 1)) * D_pad;
-      float *dst = ebuf + (t & 1) * EB;
       for (int d = ctid; d < D; d += kNT) {
         const float v = exp_r(src[d] - m);
         for (int c = 0; c < a.rep_e; ++c) dst[c * a.e_stride + d] = v;
@@ -497,10 +510,14 @@ __global__ void __launch_bounds__(kNT, 1)
       if (fail_at >= 0) {
         // remaining shifts are row maxima, remaining scales 1 (forward_backward.py:184,206)
         for (int k = fail_at + 1 + warp; k < T; k += kNW) {
-          float m = -INFINITY;
-          for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
-          m = warp_max(m);
-          if (lane == 0) shifts[k] = m;
+          if (pre) {
+            if (lane == 0) shifts[k] = Emb[k];
+          } else {
+            float m = -INFINITY;
+            for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
+            m = warp_max(m);
+            if (lane == 0) shifts[k] = m;
+          }
         }
         for (int k = fail_at + tid; k < T; k += kNT) scales[k] = 1.f;
       }

@@ -46,7 +46,8 @@ namespace {
 constexpr int kStreamThreads = 1024;
 constexpr int kMaxD = 2048;  // log-likelihood row held in registers: kMaxD / NT per thread
 constexpr float kPostScale = 268435456.f;  // 2^28: posterior bins in uint32 fixed point
-constexpr int kRingRows = 4;               // slot rows per TMA chunk (4 x 256 B)
+constexpr int kRingRows = 8;               // slot rows per TMA chunk (8 x 256 B = 2 KB)
+constexpr int kRingSlots = 2;              // chunks per warp in flight / being read
 
 struct StreamLayout {
   unsigned vec, ebuf, bins, scales, shifts, part, mpart, ring, bars, total;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   // and the wait parity is (g / nslot) & 1 across both phases.
   uint2 *ring = reinterpret_cast<uint2 *>(smem + lay.ring);
   unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
-  const int nslot = lay.nslot;
+  constexpr int nslot = kRingSlots;  // compile-time: slot = g & 1, parity = (g >> 1) & 1
   unsigned g_cons = 0, g_iss = 0, g_end = 0;  // chunks consumed / issued / phase end
   int p_i = 0, p_j = 0;                       // producer cursor: tile of this warp, row
   const uint2 *pack = nullptr;
@@ -543,17 +544,15 @@ static int launch_stream_impl2(const FBArgs<float> &a, int S32, const StreamLayo
   return check_cuda(cudaLaunchKernelEx(&cfg, kern, a, S32, lay), "fb_stream_kernel launch");
 }
 
-// TMA ring when it fits next to the columns (as many slots per warp as fit, up
-// to 4, at least 2), else slot rows straight from L2.
+// TMA ring when its kRingSlots x 2 KB per warp fit next to the columns, else
+// slot rows straight from L2.
 template <int NT, int CL>
 static int launch_stream_impl(const FBArgs<float> &a, int S32, const StreamLayout &base,
                               cudaStream_t st) {
   constexpr int NW = NT / 32;
   if (options().stream_ring) {
-    for (int ns = 4; ns >= 2; --ns) {
-      const StreamLayout lay = stream_layout(S32, a.D_pad, a.T_pad, NW, ns);
-      if (lay.total <= unsigned(kMaxSmem)) return launch_stream_impl2<NT, CL, true>(a, S32, lay, st);
-    }
+    const StreamLayout lay = stream_layout(S32, a.D_pad, a.T_pad, NW, kRingSlots);
+    if (lay.total <= unsigned(kMaxSmem)) return launch_stream_impl2<NT, CL, true>(a, S32, lay, st);
   }
   return launch_stream_impl2<NT, CL, false>(a, S32, base, st);
 }

@@ -43,11 +43,15 @@ def test_linear_forward_backward_vs_oracle(cuda, S_max, D, leak):
     rng = np.random.default_rng(S_max * 7 + D)
     B = 5
     n_phones = [S_max - 1, max(1, S_max // 2), 1, max(1, S_max // 3), max(1, S_max - 5)]
-    # T >= #phones.  Without the leak, fp32 cannot represent the final state's
-    # mass when T is far beyond the transcript (a ~e-60 binomial tail at
-    # T = 1.4 n that fp64 keeps): leak-free utterances stay close to n frames.
-    slack = (lambda n: 2 * n + 3) if leak > 0 else (lambda n: n // 4 + 3)
-    lengths = [n + int(rng.integers(0, slack(n))) for n in n_phones]
+    # T >= #phones.  Without the leak, only paths that advance on most frames
+    # reach the final state when T < ~2n, and its share of the normalised column
+    # (a binomial tail, ~e-60 at T = 1.4 n) is below fp32's range while fp64
+    # keeps it: leak-free utterances get T in [2n, 3n] (the leak, 1e-5 by
+    # default, puts lambda / S on every state each frame and removes the issue).
+    if leak > 0:
+        lengths = [n + int(rng.integers(0, 2 * n + 3)) for n in n_phones]
+    else:
+        lengths = [2 * n + int(rng.integers(0, n + 3)) for n in n_phones]
     batch = _batch(rng, lengths, D)
     graphs = _numerators(rng, n_phones, D)
     nums = P.ChainGraphBatch.from_graphs([graphs[i] for i in batch.order_map])
