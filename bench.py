@@ -334,7 +334,9 @@ def fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_loc
     x_dev = [torch.empty((max(win_rows), pool.D), dtype=torch.float32, device=dev) for _ in range(2)]
     l_dev = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(2)]
     g_dev = torch.empty((max(win_rows), pool.D), dtype=torch.float32, device=dev)
+    host_tot = torch.empty((W + args.steps, 3), dtype=torch.float64).pin_memory()
     opts = P.FBOptions()
+    host_s = []
 
     resident = None  # per-window graph batches whose device packs are already built
 
@@ -352,7 +354,8 @@ def fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_loc
             grad=g_dev[: r1 - r0])
         if pg is not None:
             torch.distributed.all_reduce(totals, group=pg)
-        return totals.to("cpu", non_blocking=True), r1 - r0
+        host_tot[i].copy_(totals, non_blocking=True)  # pinned: the host never waits
+        return None, r1 - r0
 
     def timed():
         for i in range(W):
@@ -362,9 +365,11 @@ def fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_loc
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         frames = 0
+        h0 = time.perf_counter()
         for i in range(W, W + args.steps):
             _, n = step(i)
             frames += n
+        host_s.append((time.perf_counter() - h0) / args.steps)
         t1.record(stream)
         torch.cuda.synchronize()
         ms = t0.elapsed_time(t1)
@@ -393,6 +398,7 @@ def fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_loc
            "how": "chain_loss_packed with a list of never-used ChainGraph numerators per step "
                   "(per-utterance linear records concatenated into pinned memory, one async "
                   "H2D) and a fresh window of log-likelihoods from a pinned pool"}
+    out["host_ms_per_step_issue"] = {"fresh": host_s[0] * 1e3, "resident": host_s[1] * 1e3}
     out["resident_same_windows"] = value_r
     out["vs_resident_same_windows"] = value / value_r
     if e2e:
