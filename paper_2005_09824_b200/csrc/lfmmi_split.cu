@@ -691,11 +691,12 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   if (lay.total > size_t(kMaxSmem) || size_t(2) * a.B * 4 > size_t(2) * X_pad * 4)
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "split kernel needs " + std::to_string(lay.total) + " B shared memory");
-  // Clusters: one per utterance while they fit, leaving >= 20 SMs to the
-  // numerator pass that runs beside this one (two-pass chain loss; measured on
-  // WSJ-mono: numerators 0.87 ms on all SMs, 1.26 ms on 20); beyond that LPT
-  // pairs long with short utterances.  Option split_clusters overrides.
-  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 10);
+  // Clusters: one per utterance while they fit, leaving >= 10 SMs to the
+  // numerator pass that runs beside this one (the linear-chain kernel: 0.43 ms
+  // alone, hidden behind the ~1.07 ms denominator on 10 SMs; WSJ-mono step
+  // 1.134 / 1.088 / 1.192 ms with 64 / 69 / 74 clusters, same box); beyond
+  // that LPT pairs long with short utterances.  Option split_clusters overrides.
+  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 5);
   nc = std::max(1, std::min(nc, std::min(96, sms / 2)));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > std::min(96, sms / 2))

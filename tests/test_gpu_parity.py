@@ -130,9 +130,11 @@ def _kernel_env(kernel, lib_options):
         lib_options(split=0, tile_xdb=0)
     if kernel == "numtile":
         lib_options(linear=0)
+    if kernel == "ring":  # stream kernel with its TMA slot ring (graphs beyond shared memory)
+        lib_options(stream_ring=1)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile",
+@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "ring",
                                     "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
