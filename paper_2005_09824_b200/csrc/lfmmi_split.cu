@@ -691,12 +691,13 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   if (lay.total > size_t(kMaxSmem) || size_t(2) * a.B * 4 > size_t(2) * X_pad * 4)
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "split kernel needs " + std::to_string(lay.total) + " B shared memory");
-  // Clusters: one per utterance while they fit, leaving >= 10 SMs to the
-  // numerator pass that runs beside this one (the linear-chain kernel: 0.43 ms
-  // alone, hidden behind the ~1.07 ms denominator on 10 SMs; WSJ-mono step
-  // 1.134 / 1.088 / 1.192 ms with 64 / 69 / 74 clusters, same box); beyond
-  // that LPT pairs long with short utterances.  Option split_clusters overrides.
-  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 5);
+  // Clusters: one per utterance while they fit, leaving 6 SMs to the numerator
+  // pass that runs beside this one (the linear-chain kernel: 0.43 ms alone,
+  // hidden behind the ~1.06 ms denominator; WSJ-mono step 1.111 / 1.101 / 1.088
+  // / 1.083 / 1.082 / 1.082 ms with 66 / 68 / 69 / 70 / 71 / 72 clusters, 1.19 ms
+  // with 74 — numerators then wait for free SMs); beyond that LPT pairs long
+  // with short utterances.  Option split_clusters overrides.
+  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 3);
   nc = std::max(1, std::min(nc, std::min(96, sms / 2)));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > std::min(96, sms / 2))
