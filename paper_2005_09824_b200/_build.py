@@ -31,7 +31,7 @@ TORCH_SO = os.path.join(LIB_DIR, "_lfmmi_torch" + (sysconfig.get_config_var("EXT
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CORE_SOURCES = ["lfmmi_api.cu", "lfmmi_group.cu", "lfmmi_tile.cu", "lfmmi_linear.cu", "lfmmi_stream.cu", "lfmmi_split.cu",
+CORE_SOURCES = ["lfmmi_api.cu", "lfmmi_group.cu", "lfmmi_tile.cu", "lfmmi_linear.cu", "lfmmi_stream.cu", "lfmmi_streamsplit.cu", "lfmmi_split.cu",
                 "lfmmi_graph.cpp",
                 "lfmmi_schedule.cpp", "lfmmi_fst.cpp", "lfmmi_options.cpp"]
 

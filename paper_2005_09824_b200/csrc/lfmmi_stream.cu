@@ -575,7 +575,13 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   // Two SMs per utterance (2-CTA cluster of 1024-thread CTAs) while the batch
   // leaves SMs idle, else one 1024-thread CTA per utterance.  ("512x2" — two
   // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
-  const std::string &want = options().stream_mode;  // "1024x1", "1024x2", "512x2"
+  // Default: the forward | backward split (lfmmi_streamsplit.cu) while it applies;
+  // "1024x1" / "1024x2" / "512x2" pick the single-direction kernels.
+  const std::string &want = options().stream_mode;
+  if (want == "auto" || want == "split") {
+    const int rc = launch_stream_split(a, g, st);
+    if (rc != LFMMI_ERR_UNSUPPORTED || want == "split") return rc;
+  }
   std::string mode = want != "auto" ? want : (2 * a.B <= sms ? "1024x2" : "1024x1");
   if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, S32, lay, st);
   if (mode == "512x2") return launch_stream_impl<512, 2>(a, S32, lay, st);

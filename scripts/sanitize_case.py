@@ -10,6 +10,7 @@ Cases pick the kernel under test with the library options (lfmmi_set_option):
   stream2  large-graph fb_stream_kernel<1024,2> (2-CTA cluster, DSMEM exchange)
   stream1  fb_stream_kernel<1024,1>
   ring     fb_stream_kernel<1024,1> with its TMA slot ring (cp.async.bulk + mbarrier)
+  ssplit   fb_streamsplit_kernel (forward | backward clusters, DSMEM scalars, kappa recursion)
   numtile  numerators on the generic fb_tile_kernel<128> (linear kernel disabled)
 every case also runs the linear-chain numerator kernel (except numtile) and
 the combine kernel.  Utterances are short (<= 24 frames) to keep the
@@ -35,6 +36,7 @@ CASES = {
     "stream2": ("wsj_biphone", 2, dict(stream_mode="1024x2")),
     "stream1": ("wsj_biphone", 2, dict(stream_mode="1024x1")),
     "ring": ("wsj_biphone", 2, dict(stream_mode="1024x1", stream_ring=1)),
+    "ssplit": ("wsj_biphone", 3, dict(stream_mode="split")),
     "numtile": ("wsj_mono", 3, dict(linear=0)),
 }
 

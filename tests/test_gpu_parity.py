@@ -131,7 +131,7 @@ def _kernel_env(kernel, lib_options):
     if kernel == "numtile":
         lib_options(linear=0)
     if kernel == "ring":  # stream kernel with its TMA slot ring (graphs beyond shared memory)
-        lib_options(stream_ring=1)
+        lib_options(stream_ring=1, stream_mode="1024x1")
 
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "ring",
@@ -153,7 +153,7 @@ def test_configs_vs_oracle(cuda, config, batch_size, kernel, lib_options):
     assert res.num_failed == ref.num_failed == 0
 
 
-@pytest.mark.parametrize("kernel", ["stream", "stream1", "stream512", "group"])
+@pytest.mark.parametrize("kernel", ["ssplit", "stream", "stream1", "stream512", "group"])
 def test_large_graph_l2_path_vs_oracle(cuda, kernel, lib_options):
     """Config 4 (20k states / 200k arcs / 2000 pdfs): the arc packs do not fit in
     shared memory.  "stream": coalesced 32-state tiles streamed from L2
@@ -161,6 +161,8 @@ def test_large_graph_l2_path_vs_oracle(cuda, kernel, lib_options):
     from the HBM trellis."""
     if kernel == "group":
         lib_options(stream=0)
+    if kernel == "stream":  # the single-direction kernel, 2-CTA tile split (1024x2)
+        lib_options(stream_mode="1024x2")
     if kernel == "stream1":  # one CTA per utterance instead of a 2-CTA cluster
         lib_options(stream_mode="1024x1")
     if kernel == "stream512":  # 2-CTA clusters of 512 threads (two per SM when they fit)
@@ -284,7 +286,7 @@ def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kern
     assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
 
 
-@pytest.mark.parametrize("mode", ["1024x1", "1024x2"])
+@pytest.mark.parametrize("mode", ["split", "1024x1", "1024x2"])
 def test_stream_kernel_short_utterances(cuda, mode, lib_options):
     """1-, 2- and 3-frame utterances through the L2-streamed kernel (biphone-sized
     denominator): prologue / epilogue edges of the register row pipeline."""

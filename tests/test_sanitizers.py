@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-CASES = ["split", "tile", "tile1x", "stream2", "stream1", "ring", "numtile"]
+CASES = ["split", "tile", "tile1x", "stream2", "stream1", "ring", "ssplit", "numtile"]
 
 
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
