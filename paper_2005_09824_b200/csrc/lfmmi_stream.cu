@@ -575,13 +575,12 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   // Two SMs per utterance (2-CTA cluster of 1024-thread CTAs) while the batch
   // leaves SMs idle, else one 1024-thread CTA per utterance.  ("512x2" — two
   // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
-  // Default: the forward | backward split (lfmmi_streamsplit.cu) while it applies;
-  // "1024x1" / "1024x2" / "512x2" pick the single-direction kernels.
+  // "split": the forward | backward split (lfmmi_streamsplit.cu; correct, but
+  // measured no faster: biphone 9.94 vs 9.96 ms, large 38.7 vs 30.1 ms — its
+  // frames are latency-bound on per-warp L2 slot loads like these, and doubling
+  // the SMs per utterance does not shorten them).
   const std::string &want = options().stream_mode;
-  if (want == "auto" || want == "split") {
-    const int rc = launch_stream_split(a, g, st);
-    if (rc != LFMMI_ERR_UNSUPPORTED || want == "split") return rc;
-  }
+  if (want == "split") return launch_stream_split(a, g, st);
   std::string mode = want != "auto" ? want : (2 * a.B <= sms ? "1024x2" : "1024x1");
   if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, S32, lay, st);
   if (mode == "512x2") return launch_stream_impl<512, 2>(a, S32, lay, st);

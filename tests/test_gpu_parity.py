@@ -161,8 +161,8 @@ def test_large_graph_l2_path_vs_oracle(cuda, kernel, lib_options):
     from the HBM trellis."""
     if kernel == "group":
         lib_options(stream=0)
-    if kernel == "stream":  # the single-direction kernel, 2-CTA tile split (1024x2)
-        lib_options(stream_mode="1024x2")
+    if kernel == "ssplit":  # forward | backward split (fb_streamsplit_kernel)
+        lib_options(stream_mode="split")
     if kernel == "stream1":  # one CTA per utterance instead of a 2-CTA cluster
         lib_options(stream_mode="1024x1")
     if kernel == "stream512":  # 2-CTA clusters of 512 threads (two per SM when they fit)
