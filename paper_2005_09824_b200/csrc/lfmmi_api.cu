@@ -576,12 +576,19 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
   if (!(leak >= 0.0) || !(scale_floor > 0.0))
     return set_error(LFMMI_ERR_INVALID, "leak must be >= 0 and scale_floor > 0");
   AuxStream &ax = aux_for_device();
-  const bool serial = options().serial != 0;
-  cudaStream_t nst = serial ? st : ax.aux;
-  // Two-pass path: the numerator pass (small graphs, latency-bound, one warp
-  // per utterance) runs on the auxiliary stream next to the denominator pass
-  // (one CTA per utterance).  The denominator is launched first so its CTAs
-  // claim whole SMs; the numerator warps fill the SMs it leaves free.
+  // Numerator pass beside the denominator pass (auxiliary stream) while the
+  // denominator leaves SMs free (B <= 2 x SMs: the split kernel keeps 6); when
+  // the denominator batch fills every SM (sweep: 1024 utterances), numerator
+  // warps could only run in its tail, so the numerator pass goes first on the
+  // caller's stream instead.  Option serial: -1 auto, 0 concurrent, 1 serial.
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int ser_opt = options().serial;
+  const bool serial = ser_opt > 0 || (ser_opt < 0 && batch > 2 * sms);
   // Emissions once per step, shared by the passes that take them (the linear
   // numerator kernel and the split denominator kernel).
   if (precision == LFMMI_F32 && options().emit) {
@@ -594,24 +601,39 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
     E = e;
     Em = em;
   }
-  rc = check_cuda(cudaEventRecord(ax.fork, st), "cudaEventRecord(fork)");
-  if (rc) return rc;
-  rc = forward_backward_impl(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
-                              loglikes, lengths, leak, scale_floor, den_leak_pi, total_frames,
-                              ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE, nullptr, den_log_probs,
-                              den_fail, nullptr, stream, packed, E, Em);
-  if (rc) return rc;
-  rc = check_cuda(cudaStreamWaitEvent(ax.aux, ax.fork, 0), "cudaStreamWaitEvent(fork)");
-  if (rc) return rc;
-  rc = forward_backward_impl(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
-                              loglikes, lengths, leak, scale_floor, num_leak_pi, total_frames,
-                              ws + num_off, num_bytes, ws + gam_off, LFMMI_POST_WRITE, nullptr, num_log_probs,
-                              num_fail, nullptr, nst, packed, E, Em);
-  if (rc) return rc;
-  rc = check_cuda(cudaEventRecord(ax.join, nst), "cudaEventRecord(join)");
-  if (rc) return rc;
-  rc = check_cuda(cudaStreamWaitEvent(st, ax.join, 0), "cudaStreamWaitEvent(join)");
-  if (rc) return rc;
+  auto num_pass = [&](cudaStream_t s) {
+    return forward_backward_impl(numerators, num_row_map, batch, max_frames, num_pdfs, precision,
+                                 loglikes, lengths, leak, scale_floor, num_leak_pi, total_frames,
+                                 ws + num_off, num_bytes, ws + gam_off, LFMMI_POST_WRITE, nullptr,
+                                 num_log_probs, num_fail, nullptr, s, packed, E, Em);
+  };
+  auto den_pass = [&]() {
+    return forward_backward_impl(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
+                                 loglikes, lengths, leak, scale_floor, den_leak_pi, total_frames,
+                                 ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE, nullptr,
+                                 den_log_probs, den_fail, nullptr, stream, packed, E, Em);
+  };
+  if (serial) {
+    rc = num_pass(st);
+    if (rc) return rc;
+    rc = den_pass();
+    if (rc) return rc;
+  } else {
+    // the denominator is launched first so its CTAs claim whole SMs; the
+    // numerator warps fill the SMs it leaves free
+    rc = check_cuda(cudaEventRecord(ax.fork, st), "cudaEventRecord(fork)");
+    if (rc) return rc;
+    rc = den_pass();
+    if (rc) return rc;
+    rc = check_cuda(cudaStreamWaitEvent(ax.aux, ax.fork, 0), "cudaStreamWaitEvent(fork)");
+    if (rc) return rc;
+    rc = num_pass(ax.aux);
+    if (rc) return rc;
+    rc = check_cuda(cudaEventRecord(ax.join, ax.aux), "cudaEventRecord(join)");
+    if (rc) return rc;
+    rc = check_cuda(cudaStreamWaitEvent(st, ax.join, 0), "cudaStreamWaitEvent(join)");
+    if (rc) return rc;
+  }
   {
     const dim3 grid(std::max(1, std::min(32, (max_frames * num_pdfs + 4095) / 4096)),
                     std::min(batch, 4096));

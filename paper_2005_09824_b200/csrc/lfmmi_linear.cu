@@ -31,6 +31,9 @@
 // taken from the staged row (NaN-propagating, forward_backward.py:126).
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
+#include "lfmmi_options.h"
+
+#include <algorithm>
 
 namespace lfmmi {
 namespace {
@@ -386,6 +389,412 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
   cp_async_wait<0>();
 }
 
+// ---- forward | backward split: two warps per utterance ------------------------
+//
+// Warp 0 runs the forward recursion over frames 0..T-1, warp 1 the backward one
+// over T-1..0, concurrently, meeting at h ~ T/2 (the fb_split_kernel scheme on
+// one SM): the forward warp stores alpha rows 0..h-1 and does the posteriors of
+// frames >= h, the backward warp (its own normalisers inv_t) stores beta' rows
+// h..T-1 and does the posteriors of frames < h.  The fixed-point posterior bins
+// need each frame's arc terms scaled to sum to 1 before the frame: with B_t the
+// backward column t in its own scale (raw + leak), kappa_t = sum over arcs of
+// alpha_{t-1} p e_{t-1} B_t obeys kappa_{t-1} = inv_t kappa_t scale_{t-2}
+// exactly (reference recursions), kappa_h is one dot product at the midpoint,
+// and the forward frame k >= h normalises by kappa_k / scale_{k-1}.  Emissions
+// from emit_kernel (PRE) only; K <= 8.
+struct LinSplitLayout {
+  int T4, Dr, SK;
+  size_t bytes;
+};
+
+__host__ __device__ inline LinSplitLayout lin_split_layout(int T_max, int D, int K) {
+  LinSplitLayout l;
+  l.T4 = pad4(T_max);
+  l.Dr = pad4(D);
+  l.SK = 32 * K;
+  // scales | shifts | inv (T4 + 4) | B_h (32 K) | hist[2][Dr] | ring[2][kRing][Dr] | kappa (2 doubles)
+  l.bytes = size_t(3 * l.T4 + 4 + l.SK + 2 * l.Dr + 2 * kRing * l.Dr) * 4 + 32;
+  return l;
+}
+
+template <int K>
+__device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float *lsm,
+                                                  const LinSplitLayout &lay, int b) {
+  const int lane = threadIdx.x & 31, wrole = threadIdx.x >> 5;  // 0 forward, 1 backward
+  const int D = a.D, T_max = a.T_max;
+  float *scl = lsm;                 // forward scales (tot of column t+1 at [t])
+  float *shf = lsm + lay.T4;        // row maxima
+  float *invs = lsm + 2 * lay.T4;   // backward normalisers inv_t at [t]
+  float *Bh = invs + lay.T4 + 4;    // backward column B_h at the midpoint
+  unsigned *hist = reinterpret_cast<unsigned *>(Bh + lay.SK) + wrole * lay.Dr;
+  float *ring = reinterpret_cast<float *>(Bh + lay.SK + 2 * lay.Dr) + wrole * kRing * lay.Dr;
+  double *kap = reinterpret_cast<double *>(Bh + lay.SK + 2 * lay.Dr + 2 * kRing * lay.Dr);
+  const int mode = a.mode;
+  const bool reads_post = mode == kPostAdd || mode == kPostSubtract;
+
+  long long off = 0;
+  for (int j = lane; j < b; j += 32) off += a.packed ? a.lengths[j] : item_frames(a.lengths, j, T_max);
+  off = warp_sum(off);
+  const int T = item_frames(a.lengths, b, T_max);
+  const size_t row0 = a.packed ? size_t(off) : size_t(b) * T_max;
+  const float *Lb = a.E + row0 * D;
+  const float *Emb = a.Em + row0;
+  float *post_b = a.post + row0 * D;
+  if (wrole == 0 && !reads_post && !a.packed)
+    for (size_t i = lane; i < size_t(T_max - T) * D; i += 32) post_b[size_t(T) * D + i] = 0.f;
+  if (T <= 0) {
+    if (wrole == 0) {
+      if (a.scale_logs && !a.packed)
+        for (int k = lane; k < T_max; k += 32) a.scale_logs[size_t(b) * T_max + k] = 0.0;
+      if (lane == 0) {
+        a.logp[b] = NAN;
+        a.fail[b] = 0;
+      }
+    }
+    return;  // both warps: no barriers for this item
+  }
+  const int ldt = (a.S_max + 31) & ~31;
+  float *tr = a.work + size_t(off) * ldt;
+  const bool own_row = lane * K < ldt;
+  const int h = T == 1 ? 1 : min(T - 1, max(1, (T * 33 + 32) >> 6));
+
+  const int4 item = a.g.lin_item[a.row_map[b]];
+  const int S = item.y, init = item.z;
+  const uint4 *rec = a.g.lin_state + item.x;
+  float ps[K], pin[K], fin[K];
+  unsigned pdp[K];
+  bool valid[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int s = lane * K + k;
+    valid[k] = s < S;
+    const uint4 v = valid[k] ? rec[s] : make_uint4(0u, 0u, 0u, 0u);
+    ps[k] = __uint_as_float(v.x);
+    pin[k] = __uint_as_float(v.y);
+    pdp[k] = v.z;
+    fin[k] = __uint_as_float(v.w);
+  }
+  float po_last = __shfl_down_sync(kFull, pin[0], 1);
+  unsigned pdo_last = __shfl_down_sync(kFull, pdp[0], 1) >> 16;
+  if (lane == 31) {
+    po_last = 0.f;
+    pdo_last = 0u;
+  }
+  const float leak = a.leak;
+  const float vleak = leak > 0.f ? leak / (float(S) * (1.f + leak)) : 0.f;
+  const bool vec16 = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(Lb) & 15) == 0);
+  auto stage = [&](int t) { return ring + (t % kRing) * lay.Dr; };
+  auto issue_row = [&](int t) {
+    float *dst = stage(t);
+    const float *src = Lb + size_t(t) * D;
+    if (vec16) {
+      for (int c = lane; c < (D >> 2); c += 32) cp_async_16(dst + 4 * c, src + 4 * c);
+    } else {
+      for (int d = lane; d < D; d += 32) cp_async_elem(dst + d, src + d);
+    }
+  };
+  auto load_row_k = [&](int t, float *v) {  // this lane's K entries of trellis row t
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = 0.f;
+    if (!own_row || t < 0 || t >= T) return;
+    const float *src = tr + size_t(t) * ldt + lane * K;
+    if constexpr (K >= 4) {
+#pragma unroll
+      for (int c = 0; c < K; c += 4) {
+        const float4 q = *reinterpret_cast<const float4 *>(src + c);
+        v[c] = q.x;
+        v[c + 1] = q.y;
+        v[c + 2] = q.z;
+        v[c + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < K; ++c) v[c] = src[c];
+    }
+  };
+  auto store_row_k = [&](int t, const float *v) {
+    if (!own_row) return;
+    float *dst = tr + size_t(t) * ldt + lane * K;
+    if constexpr (K >= 4) {
+#pragma unroll
+      for (int c = 0; c < K; c += 4)
+        *reinterpret_cast<float4 *>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < K; ++c) dst[c] = v[c];
+    }
+  };
+  const bool vflush = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(post_b) & 15) == 0);
+  auto flush = [&](int e) {  // this warp's bins -> gradient row e (mode), cleared
+    float *prow = post_b + size_t(e) * D;
+    if (vflush) {
+      uint4 *h4 = reinterpret_cast<uint4 *>(hist);
+      float4 *p4 = reinterpret_cast<float4 *>(prow);
+      for (int c = lane; c < (D >> 2); c += 32) {
+        const uint4 hv = h4[c];
+        h4[c] = make_uint4(0u, 0u, 0u, 0u);
+        float4 g = make_float4(float(hv.x) * kUnfix, float(hv.y) * kUnfix, float(hv.z) * kUnfix,
+                               float(hv.w) * kUnfix);
+        if (mode == kPostNegate) {
+          g = make_float4(-g.x, -g.y, -g.z, -g.w);
+        } else if (reads_post) {
+          const float4 o = p4[c];
+          const float sg = mode == kPostAdd ? 1.f : -1.f;
+          g = make_float4(o.x + sg * g.x, o.y + sg * g.y, o.z + sg * g.z, o.w + sg * g.w);
+        }
+        p4[c] = g;
+      }
+    } else {
+      for (int d = lane; d < D; d += 32) {
+        float g = float(hist[d]) * kUnfix;
+        hist[d] = 0u;
+        if (mode == kPostNegate) g = -g;
+        else if (mode == kPostAdd) g = prow[d] + g;
+        else if (mode == kPostSubtract) g = prow[d] - g;
+        prow[d] = g;
+      }
+    }
+  };
+  for (int d = lane; d < lay.Dr; d += 32) hist[d] = 0u;
+  const bool other_failed = a.other_fail != nullptr && a.other_fail[b] >= 0;
+
+  if (wrole == 0) {
+    // ======================= forward warp =========================================
+    float r[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) r[k] = (lane * K + k == init) ? 1.f : 0.f;
+    int fail_at = -1;
+    bool mid_done = false;
+    double kappa = 0.0;
+    float bcur[K];  // beta'_{t+1} of this lane's states (posterior frames)
+#pragma unroll
+    for (int k = 0; k < K; ++k) bcur[k] = 0.f;
+    auto midpoint = [&](const float *raw) {  // kappa_h = sum raw_h B_h
+      __syncthreads();  // B_h, backward rows >= h and inv_t are written
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (valid[k]) acc += double(raw[k]) * double(Bh[lane * K + k]);
+      acc = warp_sum(acc);
+      if (lane == 0) kap[0] = acc;
+      kappa = acc;
+      mid_done = true;
+      __syncthreads();  // kappa_h delivered
+    };
+#pragma unroll
+    for (int p = 0; p < kRing - 1; ++p) {
+      if (p < T) issue_row(p);
+      cp_async_commit();
+    }
+    for (int t = 0; t < T; ++t) {
+      __syncwarp();
+      if (t + kRing - 1 < T) issue_row(t + kRing - 1);
+      cp_async_commit();
+      if (t == h) {
+        midpoint(r);
+        load_row_k(t, bcur);  // row t holds beta'_{t+1}
+      }
+      cp_async_wait<kRing - 1>();
+      __syncwarp();
+      const float *Lt = stage(t);
+      float R = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) R += r[k];
+      float prev = __shfl_up_sync(kFull, r[K - 1], 1);
+      if (lane == 0) prev = 0.f;
+      R = warp_sum(R);
+      float ws[K], wi[K], A[K], Bv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ws[k] = ps[k] * Lt[pdp[k] & 0xffffu];
+        wi[k] = pin[k] * Lt[pdp[k] >> 16];
+        A[k] = ws[k] * r[k] + wi[k] * (k ? r[k - 1] : prev);
+        Bv[k] = ws[k] + wi[k];
+      }
+      float u = 1.f, v = 0.f, tot = 1.f;
+      if (t > 0) {
+        tot = R;
+        if (leak > 0.f && R > 0.f) {
+          tot = R + leak * R;
+          v = vleak;
+        }
+        if (!(tot >= a.floor_eff) || tot == INFINITY) {
+          fail_at = t - 1;
+          break;
+        }
+        u = rcp_rn(tot);
+        if (lane == 0) scl[t - 1] = tot;
+      }
+      if (lane == 0) shf[t] = Emb[t];
+      if (t < h) {  // alpha_t for the backward warp's posteriors
+        float al[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) al[k] = valid[k] ? fmaf(r[k], u, v) : 0.f;
+        store_row_k(t, al);
+      }
+      if (t >= h && !other_failed) {  // posteriors of frame t: terms / Z_t, Z_t = kappa_t / scale_{t-1}
+        const double zt = kappa / double(tot);
+        const float zs = (zt > 0.0 && zt < 1e38) ? float(1.0 / zt) : 0.f;
+        const float vprev = (lane * K > 0 && lane * K - 1 < S) ? v : 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float a_s = valid[k] ? fmaf(r[k], u, v) : 0.f;
+          const float a_p = (k ? (valid[k - 1] ? fmaf(r[k - 1], u, v) : 0.f) : fmaf(prev, u, vprev));
+          const float gs = a_s * ws[k] * bcur[k] * zs;
+          const float gi = a_p * wi[k] * bcur[k] * zs;
+          if (gs > 0.f) atomicAdd(hist + (pdp[k] & 0xffffu), __float2uint_rn(gs * kFix));
+          if (gi > 0.f) atomicAdd(hist + (pdp[k] >> 16), __float2uint_rn(gi * kFix));
+        }
+        __syncwarp();
+        flush(t);
+        __syncwarp();
+        kappa = zt / double(invs[t + 1]);  // kappa_{t+1} = Z_t / inv_{t+1}
+        if (t + 1 < T) load_row_k(t + 1, bcur);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) r[k] = fmaf(u, A[k], v * Bv[k]);
+      if (t + 1 == T) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) r[k] *= fin[k];
+      }
+    }
+    cp_async_wait<0>();
+    if (fail_at < 0) {
+      float R = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) R += r[k];
+      R = warp_sum(R);
+      const float tot = (leak > 0.f && R > 0.f) ? R + leak * R : R;
+      if (!(tot >= a.floor_eff) || tot == INFINITY)
+        fail_at = T - 1;
+      else if (lane == 0)
+        scl[T - 1] = tot;
+    }
+    if (!mid_done) {  // T == 1 (kappa_1 = scale_0) or failed before the midpoint
+      __syncwarp();
+      __syncthreads();
+      if (lane == 0) kap[0] = fail_at < 0 ? double(scl[T - 1]) : 1.0;
+      __syncthreads();
+    }
+    if (fail_at >= 0) {
+      for (int k = fail_at + 1; k < T; ++k)
+        if (lane == 0) shf[k] = Emb[k];
+      if (lane == 0)
+        for (int k = fail_at; k < T; ++k) scl[k] = 1.f;
+    }
+    __syncthreads();  // end: the backward warp's posterior rows are written
+    {
+      double acc = 0.0;
+      for (int k = lane; k < T; k += 32) {
+        const double val = log(double(scl[k])) + double(shf[k]);
+        acc += val;
+        if (a.scale_logs) a.scale_logs[size_t(b) * T_max + k] = val;
+      }
+      if (a.scale_logs)
+        for (int k = T + lane; k < T_max; k += 32) a.scale_logs[size_t(b) * T_max + k] = 0.0;
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        a.logp[b] = fail_at >= 0 ? NAN : acc;
+        a.fail[b] = fail_at;
+      }
+    }
+    if (fail_at >= 0 || other_failed)
+      for (size_t i = lane; i < size_t(T) * D; i += 32) post_b[i] = 0.f;
+  } else {
+    // ======================= backward warp ========================================
+    float Y[K];  // pre-leak column t in this warp's own scale; B_t = Y + ld_t
+#pragma unroll
+    for (int k = 0; k < K; ++k) Y[k] = fin[k] * (1.f + leak);
+    double kappa = 0.0;
+    float al[K];  // alpha of the current posterior frame (this lane's states)
+#pragma unroll
+    for (int p = 0; p < kRing - 1; ++p) {
+      const int e = T - 1 - p;
+      if (e >= 0) issue_row(e);
+      cp_async_commit();
+    }
+    for (int t = T; t >= 1; --t) {
+      const int e = t - 1;
+      __syncwarp();
+      {
+        const int en = e - (kRing - 1);
+        if (en >= 0) issue_row(en);
+        cp_async_commit();
+      }
+      if (t == h) {  // midpoint: B_h for the forward warp, then kappa_h
+        float sY = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) sY += Y[k];
+        sY = warp_sum(sY);
+        const float ldh = (t < T && leak > 0.f) ? leak * sY / float(S) : 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) Bh[lane * K + k] = valid[k] ? Y[k] + ldh : 0.f;
+        __threadfence_block();
+        __syncthreads();  // forward warp computes kappa_h
+        __syncthreads();
+        kappa = kap[0];
+        load_row_k(e, al);
+      }
+      cp_async_wait<kRing - 1>();
+      __syncwarp();
+      const float *Lt = stage(e);
+      const bool post = t <= h && !other_failed;
+      float sY = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) sY += Y[k];
+      float ynext = __shfl_down_sync(kFull, Y[0], 1);
+      if (lane == 31) ynext = 0.f;
+      float ws[K], wo[K], A[K], Bv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) ws[k] = ps[k] * Lt[pdp[k] & 0xffffu];
+#pragma unroll
+      for (int k = 0; k < K - 1; ++k) wo[k] = pin[k + 1] * Lt[pdp[k + 1] >> 16];
+      wo[K - 1] = po_last * Lt[pdo_last];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        A[k] = ws[k] * Y[k] + wo[k] * (k + 1 < K ? Y[k + 1] : ynext);
+        Bv[k] = ws[k] + wo[k];
+      }
+      sY = warp_sum(sY);
+      const float ld = (t < T && leak > 0.f) ? leak * sY / float(S) : 0.f;
+      const float n = sY + ld * float(S);
+      const float inv = (n > 0.f && n < INFINITY) ? rcp_rn(n) : 1.f;
+      if (lane == 0) invs[t] = inv;
+      if (!post) {  // beta'_t = B_t inv_t -> row e (the forward warp's posteriors)
+        if (t > h) {
+          float bb[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) bb[k] = valid[k] ? (Y[k] + ld) * inv : 0.f;
+          store_row_k(e, bb);
+        }
+      } else {  // posteriors of frame e: alpha_e p e B_t / kappa_t
+        const float zinv = (kappa > 0.0 && kappa < 1e38) ? float(1.0 / kappa) : 0.f;
+        const bool nvalid = lane * K + K < S;  // state lane K + K exists
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float bs = valid[k] ? Y[k] + ld : 0.f;
+          const float bn = k + 1 < K ? (valid[k + 1] ? Y[k + 1] + ld : 0.f)
+                                     : (nvalid ? ynext + ld : 0.f);
+          const float gs = al[k] * ws[k] * bs * zinv;
+          const float go = al[k] * wo[k] * bn * zinv;
+          if (gs > 0.f) atomicAdd(hist + (pdp[k] & 0xffffu), __float2uint_rn(gs * kFix));
+          const unsigned pdo = k + 1 < K ? (pdp[k + 1] >> 16) : pdo_last;
+          if (go > 0.f) atomicAdd(hist + pdo, __float2uint_rn(go * kFix));
+        }
+        __syncwarp();
+        flush(e);
+        __syncwarp();
+        if (t >= 2) kappa = double(inv) * kappa * double(scl[t - 2]);  // kappa_{t-1}
+        load_row_k(e - 1, al);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) Y[k] = inv * fmaf(ld, Bv[k], A[k]);
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // end
+  }
+}
+
 // One warp per utterance; this launch runs the utterances whose K lies in
 // [KLO, KHI] (the K = 16 variant needs ~2x the registers of the others, so it
 // is a separate launch that only batches with S > 256 pay for).  Shared-memory
@@ -404,6 +813,36 @@ __global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a, in
     case 8: if constexpr (KLO <= 8 && 8 <= KHI) linear_item<8, PRE>(a, lsm, lay, b); break;
     default: if constexpr (KHI >= 16) linear_item<16, PRE>(a, lsm, lay, b); break;
   }
+}
+
+// Two warps per utterance (forward | backward), utterances with K <= KMAX <= 8
+// (instantiated for the batch's largest K, so its registers follow that K).
+template <int KMAX>
+__global__ void __launch_bounds__(64) fb_linear_split_kernel(const FBArgs<float> a, int kstage) {
+  extern __shared__ __align__(16) float lsm[];
+  const int b = blockIdx.x;
+  const int K = k_of(a.g.lin_item[a.row_map[b]].y);
+  if (K > KMAX) return;
+  const LinSplitLayout lay = lin_split_layout(a.T_max, a.D, kstage);
+  switch (K) {
+    case 1: linear_item_split<1>(a, lsm, lay, b); break;
+    case 2: if constexpr (KMAX >= 2) linear_item_split<2>(a, lsm, lay, b); break;
+    case 4: if constexpr (KMAX >= 4) linear_item_split<4>(a, lsm, lay, b); break;
+    default: if constexpr (KMAX >= 8) linear_item_split<8>(a, lsm, lay, b); break;
+  }
+}
+
+template <int KMAX>
+int launch_split_k(const FBArgs<float> &a, int ks, size_t ssm, cudaStream_t st) {
+  if (ssm > 48 * 1024) {
+    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_split_kernel<KMAX>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(ssm)),
+                              "cudaFuncSetAttribute(linear split)");
+    if (rc) return rc;
+  }
+  fb_linear_split_kernel<KMAX><<<a.B, 64, ssm, st>>>(a, ks);
+  return check_cuda(cudaGetLastError(), "fb_linear_split_kernel launch");
 }
 
 template <int KLO, int KHI, bool PRE>
@@ -429,6 +868,20 @@ int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st
   const size_t smem = lin_layout(a.T_max, a.D, kstage).bytes;
   if (smem > size_t(kMaxSmem)) return LFMMI_ERR_UNSUPPORTED;
   const bool pre = a.E != nullptr;
+  if (pre && options().linear_split) {  // forward | backward warps (utterances with K <= 8)
+    const int ks = std::min(kstage, 8);
+    const size_t ssm = lin_split_layout(a.T_max, a.D, ks).bytes;
+    if (ssm <= size_t(kMaxSmem)) {
+      note_kernel(kstage <= 8 ? "fb_linear_split_kernel (forward | backward warps)"
+                              : "fb_linear_split_kernel + fb_linear_kernel<16>");
+      int rc = ks == 1   ? launch_split_k<1>(a, ks, ssm, st)
+               : ks == 2 ? launch_split_k<2>(a, ks, ssm, st)
+               : ks == 4 ? launch_split_k<4>(a, ks, ssm, st)
+                         : launch_split_k<8>(a, ks, ssm, st);
+      if (rc || kstage <= 8) return rc;
+      return launch_range<16, 16, true>(a, kstage, smem, st);
+    }
+  }
   note_kernel(kstage <= 8 ? (pre ? "fb_linear_kernel<1..8> (emissions pre-pass)"
                                  : "fb_linear_kernel<1..8>")
                           : (pre ? "fb_linear_kernel<1..8> + <16> (emissions pre-pass)"

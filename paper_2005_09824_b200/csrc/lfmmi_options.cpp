@@ -21,6 +21,7 @@ const Field kFields[] = {
     {"tile", &Options::tile, nullptr},
     {"stream", &Options::stream, nullptr},
     {"linear", &Options::linear, nullptr},
+    {"linear_split", &Options::linear_split, nullptr},
     {"split", &Options::split, nullptr},
     {"split_clusters", &Options::split_clusters, nullptr},
     {"split_h64", &Options::split_h64, nullptr},

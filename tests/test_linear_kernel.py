@@ -186,3 +186,49 @@ def test_linear_disabled_falls_back_to_tile(cuda, lib_options):
     rf = O.forward_backward(batch, nums, leak=1e-5)
     _close(fb.log_probs, rf.log_probs)
     assert not math.isnan(float(fb.log_probs[0]))
+
+
+@pytest.mark.parametrize("split", [1, 0])
+@pytest.mark.parametrize("config,batch_size,leak", [("toy", None, 1e-5), ("wsj_mono", 16, 1e-5),
+                                                    ("wsj_mono", 9, 0.0), ("wsj_mono", 9, 0.1),
+                                                    ("sweep", 6, 1e-5), ("wsj_biphone", 4, 1e-5)])
+def test_linear_split_in_chain_loss_vs_oracle(cuda, lib_options, config, batch_size, leak, split):
+    """The chain-loss numerator pass (emissions pre-pass): forward | backward warps
+    meeting at the midpoint, posteriors pre-normalised by the kappa recursion
+    (split = 1, the default), or one warp doing both (split = 0).  Sweep mixes
+    K <= 8 utterances (split kernel) with K = 16 ones (single-warp launch)."""
+    lib_options(linear_split=split)
+    w = synth.make_workload(config, seed=31, batch_size=batch_size)
+    batch, nums, den = w.build(P)
+    opts = P.FBOptions(leak_coefficient=leak)
+    res = P.chain_loss(batch, nums, den, opts)
+    ref = O.chain_loss(batch, nums, den, leak=leak)
+    assert abs(res.objective - ref.objective) <= 1e-5 * max(1.0, abs(ref.objective))
+    assert np.abs(res.grad - ref.grad).max() <= GRAD_ABS
+    for (a, _), (c, _) in zip(res.per_utt, ref.per_utt):
+        assert abs(a - c) <= 1e-5 * max(1.0, abs(c))
+    kern = str(P._backend.ext().last_kernel())
+    assert ("split" in kern) == bool(split), kern
+
+
+def test_linear_split_bitwise_batch_independent(cuda):
+    """Per-utterance K and fixed orders: a numerator's log-probability and
+    gradient rows do not depend on its batch-mates in the split kernel either."""
+    import torch
+
+    w = synth.make_workload("wsj_mono", seed=33, batch_size=10)
+    batch, nums, den = w.build(P)
+    dev = torch.device("cuda", 0)
+    seqs = [batch.values[b, :batch.lengths[b]] for b in range(10)]
+
+    def run(idx):
+        x = torch.tensor(np.concatenate([seqs[i] for i in idx]), dtype=torch.float32, device=dev)
+        ln = torch.tensor([len(seqs[i]) for i in idx], dtype=torch.int32, device=dev)
+        g, nl, _, _, _, _ = P.chain_loss_packed(x, ln, [nums.graph(i) for i in idx], den.graph(0))
+        return g.cpu().numpy(), nl.cpu().numpy()
+
+    gf, nf = run(list(range(10)))
+    gs, ns = run([3, 7])
+    offs = np.concatenate([[0], np.cumsum([len(q) for q in seqs])])
+    assert ns[0] == nf[3] and ns[1] == nf[7]
+    np.testing.assert_array_equal(gs[:len(seqs[3])], gf[offs[3]:offs[4]])
