@@ -48,9 +48,10 @@ constexpr int kMaxD = 2048;  // log-likelihood row held in registers: kMaxD / NT
 constexpr float kPostScale = 268435456.f;  // 2^28: posterior bins in uint32 fixed point
 constexpr int kRingRows = 8;               // slot rows per TMA chunk (8 x 256 B = 2 KB)
 constexpr int kRingSlots = 2;              // chunks per warp in flight / being read
+constexpr int kRingChunks = 64;            // chunk table entries per warp (per frame)
 
 struct StreamLayout {
-  unsigned vec, ebuf, bins, scales, shifts, part, mpart, ring, bars, total;
+  unsigned vec, ebuf, bins, scales, shifts, part, mpart, ring, bars, ctab, total;
   int nslot;  // TMA ring slots per warp (0: slot rows read straight from L2)
 };
 
@@ -73,6 +74,7 @@ __host__ __device__ inline StreamLayout stream_layout(int S32, int D_pad, int T_
   l.mpart = take(2u * 32u * 4u);
   l.ring = take(unsigned(NW) * unsigned(nslot) * kRingRows * 256u);
   l.bars = take(unsigned(NW) * unsigned(nslot) * 8u);
+  l.ctab = take(nslot ? unsigned(NW) * kRingChunks * 8u : 0u);
   l.total = o;
   return l;
 }
@@ -227,33 +229,38 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
   constexpr int nslot = kRingSlots;  // compile-time: slot = g & 1, parity = (g >> 1) & 1
   unsigned g_cons = 0, g_iss = 0, g_end = 0;  // chunks consumed / issued / phase end
-  int p_i = 0, p_j = 0;                       // producer cursor: tile of this warp, row
+  int p_i = 0;                                // producer cursor: chunk of this warp's table
   const uint2 *pack = nullptr;
   auto slot_ptr = [&](unsigned g) { return ring + (size_t(warp) * nslot + g % nslot) * (kRingRows * 32); };
   auto slot_bar = [&](unsigned g) { return bars + warp * nslot + g % nslot; };
-  auto issue = [&]() {  // warp-converged: next chunk of the cursor into its slot
-    int trips = __shfl_sync(kFull, my_trips, p_i);
-    while (p_j >= trips) {  // skip empty tiles (wrapping to the next frame)
-      p_j = 0;
-      if (++p_i == ntw) p_i = 0;
-      trips = __shfl_sync(kFull, my_trips, p_i);
-    }
-    const int base = __shfl_sync(kFull, my_base, p_i);
-    const int n = min(kRingRows, trips - p_j);
+  // This warp's chunks of one frame, in consumption order, as {slot offset into
+  // the pack, bytes} — built once per phase so the producer (lane 0) is a table
+  // read plus the bulk copy.
+  uint2 *ctab = reinterpret_cast<uint2 *>(smem + lay.ctab) + size_t(warp) * kRingChunks;
+  int nchunk = 0;
+  auto issue = [&]() {
     if (lane == 0) {
+      const uint2 ent = ctab[p_i];
       fence_proxy_async_smem();
-      bulk_copy_g2s(slot_ptr(g_iss), pack + base + 32 * p_j, unsigned(n) * 256u, slot_bar(g_iss));
+      bulk_copy_g2s(slot_ptr(g_iss), pack + ent.x, ent.y, slot_bar(g_iss));
     }
     ++g_iss;
-    p_j += kRingRows;
+    if (++p_i == nchunk) p_i = 0;
   };
   auto begin_phase = [&](const uint2 *pk, int frames) {
     if constexpr (RING) {
       pack = pk;
       p_i = 0;
-      p_j = 0;
       int c = 0;
-      for (int i = 0; i < ntw; ++i) c += (__shfl_sync(kFull, my_trips, i) + kRingRows - 1) / kRingRows;
+      for (int i = 0; i < ntw; ++i) {
+        const int tr = __shfl_sync(kFull, my_trips, i);
+        const int bs = __shfl_sync(kFull, my_base, i);
+        for (int j0 = 0; j0 < tr; j0 += kRingRows, ++c)
+          if (lane == 0 && c < kRingChunks)
+            ctab[c] = make_uint2(unsigned(bs + 32 * j0), unsigned(min(kRingRows, tr - j0)) * 256u);
+      }
+      nchunk = c;  // (the launcher guarantees c <= kRingChunks)
+      __syncwarp();
       g_end = g_iss + unsigned(c) * unsigned(frames);
       for (int q = 0; q < nslot && g_iss < g_end; ++q) issue();
     }
@@ -547,10 +554,14 @@ static int launch_stream_impl2(const FBArgs<float> &a, int S32, const StreamLayo
 // TMA ring when its kRingSlots x 2 KB per warp fit next to the columns, else
 // slot rows straight from L2.
 template <int NT, int CL>
-static int launch_stream_impl(const FBArgs<float> &a, int S32, const StreamLayout &base,
-                              cudaStream_t st) {
+static int launch_stream_impl(const FBArgs<float> &a, const lfmmi_graphs *g, int S32,
+                              const StreamLayout &base, cudaStream_t st) {
   constexpr int NW = NT / 32;
-  if (options().stream_ring) {
+  // per warp and frame: <= ceil(tiles / (CL NW)) tiles of <= max_deg rows
+  const int tiles_per_warp = (g->max_stiles + CL * NW - 1) / (CL * NW);
+  const int max_deg = std::max(g->max_in_deg, g->max_out_deg);
+  const bool fits = tiles_per_warp * ((max_deg + kRingRows - 1) / kRingRows) <= kRingChunks;
+  if (options().stream_ring && fits) {
     const StreamLayout lay = stream_layout(S32, a.D_pad, a.T_pad, NW, kRingSlots);
     if (lay.total <= unsigned(kMaxSmem)) return launch_stream_impl2<NT, CL, true>(a, S32, lay, st);
   }
@@ -582,9 +593,9 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   const std::string &want = options().stream_mode;
   if (want == "split") return launch_stream_split(a, g, st);
   std::string mode = want != "auto" ? want : (2 * a.B <= sms ? "1024x2" : "1024x1");
-  if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, S32, lay, st);
-  if (mode == "512x2") return launch_stream_impl<512, 2>(a, S32, lay, st);
-  return launch_stream_impl<1024, 1>(a, S32, lay, st);
+  if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, g, S32, lay, st);
+  if (mode == "512x2") return launch_stream_impl<512, 2>(a, g, S32, lay, st);
+  return launch_stream_impl<1024, 1>(a, g, S32, lay, st);
 }
 
 template int launch_stream<double>(const FBArgs<double> &, const lfmmi_graphs *, cudaStream_t);
