@@ -417,6 +417,11 @@ __host__ __device__ inline LinSplitLayout lin_split_layout(int T_max, int D, int
   return l;
 }
 
+// The two warps of a split utterance meet at different code locations (the
+// forward warp inside its frame loop, the backward warp at its midpoint), so
+// they use the non-aligned named barrier 1 (64 threads), not __syncthreads.
+__device__ __forceinline__ void pair_sync() { asm volatile("barrier.sync 1, 64;\n" ::: "memory"); }
+
 template <int K>
 __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float *lsm,
                                                   const LinSplitLayout &lay, int b) {
@@ -570,7 +575,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
 #pragma unroll
     for (int k = 0; k < K; ++k) bcur[k] = 0.f;
     auto midpoint = [&](const float *raw) {  // kappa_h = sum raw_h B_h
-      __syncthreads();  // B_h, backward rows >= h and inv_t are written
+      pair_sync();  // B_h, backward rows >= h and inv_t are written
       double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k)
@@ -579,7 +584,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       if (lane == 0) kap[0] = acc;
       kappa = acc;
       mid_done = true;
-      __syncthreads();  // kappa_h delivered
+      pair_sync();  // kappa_h delivered
     };
 #pragma unroll
     for (int p = 0; p < kRing - 1; ++p) {
@@ -672,9 +677,9 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
     }
     if (!mid_done) {  // T == 1 (kappa_1 = scale_0) or failed before the midpoint
       __syncwarp();
-      __syncthreads();
+      pair_sync();
       if (lane == 0) kap[0] = fail_at < 0 ? double(scl[T - 1]) : 1.0;
-      __syncthreads();
+      pair_sync();
     }
     if (fail_at >= 0) {
       for (int k = fail_at + 1; k < T; ++k)
@@ -682,7 +687,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       if (lane == 0)
         for (int k = fail_at; k < T; ++k) scl[k] = 1.f;
     }
-    __syncthreads();  // end: the backward warp's posterior rows are written
+    pair_sync();  // end: the backward warp's posterior rows are written
     {
       double acc = 0.0;
       for (int k = lane; k < T; k += 32) {
@@ -730,8 +735,8 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
 #pragma unroll
         for (int k = 0; k < K; ++k) Bh[lane * K + k] = valid[k] ? Y[k] + ldh : 0.f;
         __threadfence_block();
-        __syncthreads();  // forward warp computes kappa_h
-        __syncthreads();
+        pair_sync();  // forward warp computes kappa_h
+        pair_sync();
         kappa = kap[0];
         load_row_k(e, al);
       }
@@ -791,7 +796,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       for (int k = 0; k < K; ++k) Y[k] = inv * fmaf(ld, Bv[k], A[k]);
     }
     cp_async_wait<0>();
-    __syncthreads();  // end
+    pair_sync();  // end
   }
 }
 

@@ -21,7 +21,7 @@ struct Options {
   int stream_ring = 0;    // stream kernel: TMA slot ring (measured slower: issue-bound)
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
   int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots
-  int serial = -1;        // chain_loss: numerator pass before the den pass (-1 auto: B > 2 x SMs)
+  int serial = 0;         // chain_loss: numerator pass before the den pass (-1 auto: B > 2 x SMs)
   int emit = 1;           // chain_loss (fp32): emissions pre-pass shared by the passes
   int sched_iters = -1;   // bank-conflict local search moves per slot row (-1 auto)
   int chore_bias = 16;    // den warp lists: extra slot rows charged to the chore warps (pack time)
