@@ -166,3 +166,59 @@ def test_synthetic_recipe_deterministic():
     assert a.total_frames == 28778  # SURVEY.md §6 calibration draw
     for x in a.seqs[:4]:
         assert np.array_equal(x, x.astype(np.float32).astype(np.float64))
+
+
+# ------------------------------------------------- options + linear records
+def test_options_struct_roundtrip():
+    """One options struct (lfmmi_set_option / lfmmi_get_option / reset), no env reads."""
+    lib = ctypes.CDLL(_build.CORE_SO)
+    lib.lfmmi_last_error.restype = ctypes.c_char_p
+    buf = ctypes.create_string_buffer(64)
+    try:
+        assert lib.lfmmi_set_option(b"split_clusters", b"42") == 0
+        assert lib.lfmmi_get_option(b"split_clusters", buf, 64) == 0 and buf.value == b"42"
+        assert lib.lfmmi_set_option(b"stream_mode", b"1024x1") == 0
+        assert lib.lfmmi_get_option(b"stream_mode", buf, 64) == 0 and buf.value == b"1024x1"
+        assert lib.lfmmi_set_option(b"no_such_option", b"1") == 1
+        assert b"unknown option" in lib.lfmmi_last_error()
+        assert lib.lfmmi_set_option(b"split", b"x") == 1  # integers only
+    finally:
+        lib.lfmmi_reset_options()
+    assert lib.lfmmi_get_option(b"split_clusters", buf, 64) == 0 and buf.value == b"0"
+    with _backend.options(split=0, linear_split=0):
+        assert _backend.ext().get_option("split") == "0"
+    assert _backend.ext().get_option("split") == "-1"
+
+
+def test_create_linear_validates_before_device_use():
+    lib = ctypes.CDLL(_build.CORE_SO)
+    lib.lfmmi_last_error.restype = ctypes.c_char_p
+    out = ctypes.c_void_p()
+    assert lib.lfmmi_graphs_create_linear(4, 600, 84, None, None, ctypes.byref(out)) == 1
+    assert b"max_states" in lib.lfmmi_last_error()
+    assert lib.lfmmi_graphs_create_linear(4, 100, 84, None, None, ctypes.byref(out)) == 1
+    assert b"NULL" in lib.lfmmi_last_error()
+
+
+def test_linear_records_of_reference_numerators():
+    """Per-utterance records (graph.linear_records) of the reference's own
+    build_numerator graphs: one record per state with the self-loop and entry
+    arcs of toy_builder.py:218-265; other graph shapes return None."""
+    from paper_2005_09824_b200.graph import linear_records
+
+    rng = np.random.default_rng(0)
+    phones = rng.integers(0, 42, 30).tolist()
+    arcs, S, fin = synth.numerator_arcs(phones, 42)
+    g = P.ChainGraph(arcs, S, 84, 0, fin)
+    rec = linear_records(g)
+    assert rec.shape == (S, 4) and rec.dtype == np.uint32
+    f32 = rec.view(np.float32)
+    assert f32[0, 0] == 0 and f32[1, 1] == 1.0 and f32[1, 0] == 0.5  # entry 1.0, self-loop 0.5
+    assert (rec[1, 2] & 0xFFFF) == 2 * phones[0] + 1 and (rec[1, 2] >> 16) == 2 * phones[0]
+    assert f32[S - 1, 3] == 0.5 and np.all(f32[:-1, 3] == 0)
+    ring = P.ChainGraph([(0, 1, 0, 1.0), (1, 0, 1, 0.5)], 2, 2, 0, [0.0, 0.5])
+    assert linear_records(ring) is None  # a backward arc: not a linear chain
+    C = _reference()
+    topo = C.PhoneTopology(42)
+    ref_g = C.build_numerator(phones, topo)
+    np.testing.assert_array_equal(linear_records(ref_g), rec)
