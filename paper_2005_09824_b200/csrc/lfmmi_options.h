@@ -18,7 +18,7 @@ struct Options {
   int split_clusters = 0; // 0 = auto
   int split_h64 = 33;     // split midpoint in 64ths of T
   std::string stream_mode = "auto";  // "auto" | "1024x1" | "1024x2" | "512x2"
-  int stream_ring = 0;    // stream kernel: TMA slot ring (measured slower: issue-bound)
+  int stream_ring = 1;    // stream kernel: TMA slot ring when it fits (biphone 9.45 vs 9.96 ms)
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
   int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots
   int serial = 0;         // chain_loss: numerator pass before the den pass (-1 auto: B > 2 x SMs)

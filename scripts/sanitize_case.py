@@ -8,7 +8,7 @@ Cases pick the kernel under test with the library options (lfmmi_set_option):
   tile     denominator fb_tile_kernel<512> with double-buffered posterior slots (XDB)
   tile1x   ... single slot buffer
   stream2  large-graph fb_stream_kernel<1024,2> (2-CTA cluster, DSMEM exchange)
-  stream1  fb_stream_kernel<1024,1>
+  stream1  fb_stream_kernel<1024,1> reading slot rows straight from L2
   ring     fb_stream_kernel<1024,1> with its TMA slot ring (cp.async.bulk + mbarrier)
   ssplit   fb_streamsplit_kernel (forward | backward clusters, DSMEM scalars, kappa recursion)
   numtile  numerators on the generic fb_tile_kernel<128> (linear kernel disabled)
@@ -34,7 +34,7 @@ CASES = {
     "tile": ("wsj_mono", 3, dict(split=0)),
     "tile1x": ("wsj_mono", 3, dict(split=0, tile_xdb=0)),
     "stream2": ("wsj_biphone", 2, dict(stream_mode="1024x2")),
-    "stream1": ("wsj_biphone", 2, dict(stream_mode="1024x1")),
+    "stream1": ("wsj_biphone", 2, dict(stream_mode="1024x1", stream_ring=0)),
     "ring": ("wsj_biphone", 2, dict(stream_mode="1024x1", stream_ring=1)),
     "ssplit": ("wsj_biphone", 3, dict(stream_mode="split")),
     "numtile": ("wsj_mono", 3, dict(linear=0)),

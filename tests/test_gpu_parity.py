@@ -130,11 +130,11 @@ def _kernel_env(kernel, lib_options):
         lib_options(split=0, tile_xdb=0)
     if kernel == "numtile":
         lib_options(linear=0)
-    if kernel == "ring":  # stream kernel with its TMA slot ring (graphs beyond shared memory)
-        lib_options(stream_ring=1, stream_mode="1024x1")
+    if kernel == "noring":  # stream kernel reading slot rows straight from L2 (no TMA ring)
+        lib_options(stream_ring=0, stream_mode="1024x1")
 
 
-@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "ring",
+@pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "noring",
                                     "group"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
