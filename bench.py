@@ -298,6 +298,36 @@ def numpy_api_leg(P, batch, nums, den, args):
                    "memory returned as numpy; host wall clock, synchronous API"}
 
 
+def fp64_leg(P, values, lengths, nums, den, opts, frames, flush, stream, args):
+    """The same step in fp64 (the reference's arithmetic): f64 instantiations of
+    the generic tile / linear-fallback kernels, device-resident inputs."""
+    import torch
+
+    v64 = values.double()
+    g64 = torch.empty_like(v64)
+    step = lambda: P.chain_loss_device(v64, lengths, nums, den, opts, total_frames=frames,  # noqa: E731
+                                       grad=g64)
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    n = max(2, min(args.steps, 5))
+    ms = []
+    for _ in range(n):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    ms_step = float(np.mean(ms))
+    del v64, g64
+    return {"value": frames / (ms_step / 1e3), "unit": "frames/s", "ms_per_step": ms_step,
+            "den_kernel": str(P._backend.ext().last_den_kernel()), "steps": n,
+            "how": "chain_loss_device on float64 inputs (what the fp32 production path is "
+                   "compared against); L2 flushed before each step"}
+
+
 def fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_local, e2e):
     """Training-loop leg: every step draws a NEW set of numerator ChainGraph
     objects (never used in a loss before, from a pool built up front as a data
@@ -636,11 +666,12 @@ def run_ours(args):
                       "double-buffered) + D2H of the step's totals on a read-back stream; "
                       "grad stays on device"}
 
-    e2e_numpy = e2e_fresh = None
+    e2e_numpy = e2e_fresh = fp64 = None
     if not args.no_e2e and not args.no_extra_e2e and not args.profile:
         e2e_numpy = numpy_api_leg(P, batch, nums, den, args)
         e2e_fresh = fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_local,
                                         e2e)
+        fp64 = fp64_leg(P, values, lengths, nums, den, opts, frames_local, flush, stream, args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -667,6 +698,7 @@ def run_ours(args):
                          "peak_source": peak_src},
             "kernel_share_of_step": kernel_ms / ms_per_step,
             "e2e": e2e, "e2e_numpy_api": e2e_numpy, "e2e_fresh_numerators": e2e_fresh,
+            "fp64_device": fp64,
             "gpu_launches": launches_per_step * args.steps, "cpu_baseline": cpu,
             "clocks": clocks, "nccl": nccl,
         }
