@@ -820,33 +820,35 @@ __global__ void __launch_bounds__(32) fb_linear_kernel(const FBArgs<float> a, in
   }
 }
 
-// Two warps per utterance (forward | backward), utterances with K <= KMAX <= 8
-// (instantiated for the batch's largest K, so its registers follow that K).
-template <int KMAX>
+// Two warps per utterance (forward | backward) for the utterances with K in
+// [KLO, KHI]: instantiated for the batch's largest K <= 8 (registers follow that
+// K), plus a K = 16 launch (254 registers) only when the batch has S > 256.
+template <int KLO, int KHI>
 __global__ void __launch_bounds__(64) fb_linear_split_kernel(const FBArgs<float> a, int kstage) {
   extern __shared__ __align__(16) float lsm[];
   const int b = blockIdx.x;
   const int K = k_of(a.g.lin_item[a.row_map[b]].y);
-  if (K > KMAX) return;
+  if (K < KLO || K > KHI) return;
   const LinSplitLayout lay = lin_split_layout(a.T_max, a.D, kstage);
   switch (K) {
-    case 1: linear_item_split<1>(a, lsm, lay, b); break;
-    case 2: if constexpr (KMAX >= 2) linear_item_split<2>(a, lsm, lay, b); break;
-    case 4: if constexpr (KMAX >= 4) linear_item_split<4>(a, lsm, lay, b); break;
-    default: if constexpr (KMAX >= 8) linear_item_split<8>(a, lsm, lay, b); break;
+    case 1: if constexpr (KLO <= 1) linear_item_split<1>(a, lsm, lay, b); break;
+    case 2: if constexpr (KLO <= 2 && KHI >= 2) linear_item_split<2>(a, lsm, lay, b); break;
+    case 4: if constexpr (KLO <= 4 && KHI >= 4) linear_item_split<4>(a, lsm, lay, b); break;
+    case 8: if constexpr (KLO <= 8 && KHI >= 8) linear_item_split<8>(a, lsm, lay, b); break;
+    default: if constexpr (KHI >= 16) linear_item_split<16>(a, lsm, lay, b); break;
   }
 }
 
-template <int KMAX>
+template <int KLO, int KHI>
 int launch_split_k(const FBArgs<float> &a, int ks, size_t ssm, cudaStream_t st) {
   if (ssm > 48 * 1024) {
-    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_split_kernel<KMAX>,
+    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_split_kernel<KLO, KHI>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    int(ssm)),
                               "cudaFuncSetAttribute(linear split)");
     if (rc) return rc;
   }
-  fb_linear_split_kernel<KMAX><<<a.B, 64, ssm, st>>>(a, ks);
+  fb_linear_split_kernel<KLO, KHI><<<a.B, 64, ssm, st>>>(a, ks);
   return check_cuda(cudaGetLastError(), "fb_linear_split_kernel launch");
 }
 
@@ -873,18 +875,16 @@ int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st
   const size_t smem = lin_layout(a.T_max, a.D, kstage).bytes;
   if (smem > size_t(kMaxSmem)) return LFMMI_ERR_UNSUPPORTED;
   const bool pre = a.E != nullptr;
-  if (pre && options().linear_split) {  // forward | backward warps (utterances with K <= 8)
-    const int ks = std::min(kstage, 8);
-    const size_t ssm = lin_split_layout(a.T_max, a.D, ks).bytes;
+  if (pre && options().linear_split) {  // forward | backward warps
+    const size_t ssm = lin_split_layout(a.T_max, a.D, kstage).bytes;
     if (ssm <= size_t(kMaxSmem)) {
-      note_kernel(kstage <= 8 ? "fb_linear_split_kernel (forward | backward warps)"
-                              : "fb_linear_split_kernel + fb_linear_kernel<16>");
-      int rc = ks == 1   ? launch_split_k<1>(a, ks, ssm, st)
-               : ks == 2 ? launch_split_k<2>(a, ks, ssm, st)
-               : ks == 4 ? launch_split_k<4>(a, ks, ssm, st)
-                         : launch_split_k<8>(a, ks, ssm, st);
+      note_kernel("fb_linear_split_kernel (forward | backward warps)");
+      int rc = kstage == 1   ? launch_split_k<1, 1>(a, kstage, ssm, st)
+               : kstage == 2 ? launch_split_k<1, 2>(a, kstage, ssm, st)
+               : kstage == 4 ? launch_split_k<1, 4>(a, kstage, ssm, st)
+                             : launch_split_k<1, 8>(a, kstage, ssm, st);
       if (rc || kstage <= 8) return rc;
-      return launch_range<16, 16, true>(a, kstage, smem, st);
+      return launch_split_k<16, 16>(a, kstage, ssm, st);
     }
   }
   note_kernel(kstage <= 8 ? (pre ? "fb_linear_kernel<1..8> (emissions pre-pass)"
