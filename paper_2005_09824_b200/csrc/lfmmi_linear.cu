@@ -879,6 +879,10 @@ int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st
     const size_t ssm = lin_split_layout(a.T_max, a.D, kstage).bytes;
     if (ssm <= size_t(kMaxSmem)) {
       note_kernel("fb_linear_split_kernel (forward | backward warps)");
+      // K = 16 in the batch: one launch for every K (252 registers for all, but
+      // the long and short transcripts share the SMs), or (option
+      // linear_k16 = 0) a K <= 8 launch followed by a K = 16 one
+      if (kstage > 8 && options().linear_k16) return launch_split_k<1, 16>(a, kstage, ssm, st);
       int rc = kstage == 1   ? launch_split_k<1, 1>(a, kstage, ssm, st)
                : kstage == 2 ? launch_split_k<1, 2>(a, kstage, ssm, st)
                : kstage == 4 ? launch_split_k<1, 4>(a, kstage, ssm, st)
