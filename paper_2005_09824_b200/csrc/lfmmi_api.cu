@@ -225,8 +225,10 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
               const void *L, const int *lengths, double leak, double floor, const void *leak_pi,
               void *work, size_t work_bytes, void *post, int mode, const int *other_fail,
               double *logp, int *fail, double *scale_logs, cudaStream_t st, bool packed,
-              int64_t total_frames, const Real *E = nullptr, const Real *Em = nullptr) {
+              int64_t total_frames, const Real *E = nullptr, const Real *Em = nullptr,
+              int reserve_sms = 0) {
   FBArgs<Real> a{};
+  a.reserve_sms = reserve_sms;
   a.E = E;
   a.Em = Em;
   a.g = graphs->dev;
@@ -338,7 +340,8 @@ static int forward_backward_impl(const lfmmi_graphs *graphs, const int64_t *row_
                                       int32_t post_mode, const int32_t *other_fail,
                                       double *log_probs, int32_t *fail_frames,
                                       double *scale_logs, void *stream, bool packed,
-                                      const float *E = nullptr, const float *Em = nullptr) {
+                                      const float *E = nullptr, const float *Em = nullptr,
+                                      int reserve_sms = 0) {
   int rc = check_common(graphs, batch, max_frames, num_pdfs, precision);
   if (rc) return rc;
   if (!row_map || !loglikes || !lengths || !workspace || !posteriors || !log_probs || !fail_frames)
@@ -360,7 +363,7 @@ static int forward_backward_impl(const lfmmi_graphs *graphs, const int64_t *row_
   return run_fused<float>(graphs, row_map, batch, max_frames, num_pdfs, loglikes, lengths, leak,
                           scale_floor, leak_pi, workspace, workspace_bytes, posteriors, post_mode,
                           other_fail, log_probs, fail_frames, scale_logs, st, packed,
-                          total_frames, E, Em);
+                          total_frames, E, Em, reserve_sms);
 }
 
 
@@ -588,6 +591,12 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  // SMs the split denominator leaves to the concurrent numerator pass, by the
+  // numerators' size (their per-utterance latency grows with the states per
+  // lane).  Sweep at B = 128 (S up to 501): step 5.54 / 5.18 / 4.00 / 4.23 /
+  // 4.55 ms with 71 / 68 / 64 / 60 / 56 clusters (6 / 12 / 20 / 28 / 36 SMs left).
+  const int ns = numerators->max_states;
+  const int num_reserve = ns <= 128 ? 6 : ns <= 256 ? 10 : 20;
   const int ser_opt = options().serial;
   const bool serial = ser_opt > 0 || (ser_opt < 0 && batch > 2 * sms);
   // Emissions once per step, shared by the passes that take them (the linear
@@ -612,7 +621,8 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
     return forward_backward_impl(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
                                  loglikes, lengths, leak, scale_floor, den_leak_pi, total_frames,
                                  ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE, nullptr,
-                                 den_log_probs, den_fail, nullptr, stream, packed, E, Em);
+                                 den_log_probs, den_fail, nullptr, stream, packed, E, Em,
+                                 num_reserve);
   };
   if (serial) {
     rc = num_pass(st);

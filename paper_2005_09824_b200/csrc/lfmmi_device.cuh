@@ -158,6 +158,7 @@ struct FBArgs {
   // in L's layout and the row maxima m ((B, T_max) padded / (sum T) packed), or NULL.
   const Real *E;
   const Real *Em;
+  int reserve_sms;  // split den kernel: SMs to leave to the concurrent numerator pass (0: default)
 };
 
 }  // namespace lfmmi

@@ -879,9 +879,10 @@ int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st
     const size_t ssm = lin_split_layout(a.T_max, a.D, kstage).bytes;
     if (ssm <= size_t(kMaxSmem)) {
       note_kernel("fb_linear_split_kernel (forward | backward warps)");
-      // K = 16 in the batch: one launch for every K (252 registers for all, but
-      // the long and short transcripts share the SMs), or (option
-      // linear_k16 = 0) a K <= 8 launch followed by a K = 16 one
+      // K = 16 in the batch: a K <= 8 launch followed by a K = 16 one (252
+      // registers only for the long transcripts), or (option linear_k16 = 1)
+      // one launch for every K.  Sweep at B = 128 (the 8-GPU per-rank load):
+      // step 4.00 vs 4.31 ms; at B = 1024: 28.6 vs 28.2 ms.
       if (kstage > 8 && options().linear_k16) return launch_split_k<1, 16>(a, kstage, ssm, st);
       int rc = kstage == 1   ? launch_split_k<1, 1>(a, kstage, ssm, st)
                : kstage == 2 ? launch_split_k<1, 2>(a, kstage, ssm, st)

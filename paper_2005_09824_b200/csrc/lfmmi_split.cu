@@ -697,7 +697,8 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   // / 1.083 / 1.082 / 1.082 ms with 66 / 68 / 69 / 70 / 71 / 72 clusters, 1.19 ms
   // with 74 — numerators then wait for free SMs); beyond that LPT pairs long
   // with short utterances.  Option split_clusters overrides.
-  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 3);
+  const int reserve = a.reserve_sms > 0 ? a.reserve_sms : 6;
+  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, (sms - reserve) / 2);
   nc = std::max(1, std::min(nc, std::min(96, sms / 2)));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > std::min(96, sms / 2))
