@@ -533,3 +533,81 @@ def test_chain_loss_exact_workspace_concurrent_repeat(cuda):
     with pytest.raises(ValueError, match="workspace"):
         ext.chain_loss(ng.handle, ng.row_map, dg.handle, dg.row_map, values, lengths, 1e-5,
                        1e-300, None, None, tf, ws[:-1024], grad, nl, dl, nf, df, tot)
+
+
+def test_chain_loss_module_ragged_steps(cuda):
+    """ChainLoss over several training steps with ragged (sum T, D) input and
+    a plain list of numerator graphs: batch size from input_lengths (not sum T),
+    one resident denominator pack, bounded caches, loss/grad vs the oracle."""
+    import torch
+
+    from paper_2005_09824_b200 import graph as G
+
+    w = synth.make_workload("wsj_mono", seed=41, batch_size=24)
+    batch, nums, den = w.build(P)
+    mod = P.ChainLoss(den.graph(0))
+    packs_before = len(G._GRAPH_PACKS)
+    for step, idx in enumerate([range(0, 8), range(8, 16), range(16, 24), range(4, 12)]):
+        idx = list(idx)
+        seqs = [batch.values[b, :batch.lengths[b]] for b in idx]
+        x = torch.tensor(np.concatenate(seqs), dtype=torch.float32, device="cuda",
+                         requires_grad=True)
+        lens = torch.tensor([len(q) for q in seqs], dtype=torch.int32)
+        loss = mod(x, lens, [nums.graph(b) for b in idx])
+        loss.backward()
+        sub = P.make_batch(seqs)
+        sn = [nums.graph(idx[j]) for j in sub.order_map]
+        ref = O.chain_loss(sub, P.ChainGraphBatch.from_graphs(sn),
+                           P.ChainGraphBatch.broadcast(den.graph(0), len(idx)), leak=1e-5)
+        assert _rel(float(loss.detach()), ref.loss) <= FP32_OBJ_REL, step
+        g = x.grad.double().cpu().numpy()
+        frames = int(sub.lengths.sum())
+        offs = np.concatenate([[0], np.cumsum([len(q) for q in seqs])])
+        for k, j in enumerate(sub.order_map):  # sorted item k is idx[j]
+            exp = -ref.grad[k, :sub.lengths[k]] / frames
+            assert np.abs(g[offs[j]:offs[j + 1]] - exp).max() <= FP32_GRAD_ABS, step
+    assert len(mod._den_cache) == 1  # one batch size (8) -> one broadcast batch
+    assert len(G._GRAPH_PACKS) - packs_before <= 1  # one resident den pack
+
+
+def test_chain_function_all_failed_gives_zero_grad(cuda):
+    """Every utterance failing (NaN input) gives loss 0 and a zero gradient,
+    never NaN into the model (ADVICE: 0 * inf); chain_loss raises as the
+    reference does (loss.py:63-64)."""
+    import torch
+
+    w = synth.make_workload("wsj_mono", seed=42, batch_size=3)
+    batch, nums, den = w.build(P)
+    x = torch.full((batch.batch_size, batch.max_length, w.D), float("nan"), device="cuda",
+                   requires_grad=True)
+    lens = torch.tensor(batch.lengths, dtype=torch.int32)
+    loss = P.ChainFunction.apply(x, lens, nums, den)
+    loss.backward()
+    assert float(loss.detach()) == 0.0
+    assert torch.all(x.grad == 0)
+    values = np.full(batch.values.shape, np.nan)
+    bad = P.LogLikBatch(values=values, lengths=batch.lengths,
+                        valid_batch_sizes=batch.valid_batch_sizes, order_map=batch.order_map)
+    with pytest.raises(RuntimeError, match="failed"):
+        P.chain_loss(bad, nums, den)
+
+
+def test_bad_lengths_fail_items_instead_of_faulting(cuda):
+    """A length beyond T_max (e.g. pre-subsampling lengths) marks that item failed
+    on the device instead of writing out of bounds; a wrong-sized lengths or
+    numerator list raises before launch."""
+    import torch
+
+    w = synth.make_workload("wsj_mono", seed=43, batch_size=4)
+    batch, nums, den = w.build(P)
+    x = torch.tensor(batch.values, dtype=torch.float32, device="cuda")
+    lens = torch.tensor(batch.lengths, dtype=torch.int32, device="cuda")
+    lens[1] = batch.max_length + 100
+    g, nl, dl, nf, df, tot = P.chain_loss_device(x, lens, nums, den)
+    torch.cuda.synchronize()
+    assert int(df[1]) >= 0 and int(round(float(tot[2]))) == 1
+    assert torch.all(g[1] == 0)
+    with pytest.raises((ValueError, RuntimeError)):
+        P.chain_loss_device(x, lens[:3], nums, den)
+    with pytest.raises(ValueError, match="batch has"):
+        P.chain_loss_device(x[:3], lens[:3], nums, den)
