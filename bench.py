@@ -476,6 +476,10 @@ def run_ours(args):
     from paper_2005_09824_b200 import _backend, synth
 
     rank, world, local = dist_env()
+    # one process per GPU; BENCH_BACKEND=gloo lets N ranks share fewer GPUs
+    # (plumbing test of the N > 1 path on a 1-GPU box; NCCL needs distinct GPUs)
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -485,7 +489,10 @@ def run_ours(args):
         # communicator set-up lines into a per-process file (summarised in the JSON)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_FILE", NCCL_LOG)
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist.group.WORLD
     ext = _backend.require_cuda()
 
@@ -701,6 +708,7 @@ def run_ours(args):
             "fp64_device": fp64,
             "gpu_launches": launches_per_step * args.steps, "cpu_baseline": cpu,
             "clocks": clocks, "nccl": nccl,
+            "process_group": (os.environ.get("BENCH_BACKEND", "nccl") if world > 1 else None),
         }
         print(json.dumps(line), flush=True)
     if pg is not None:
