@@ -213,7 +213,11 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
       u = rcp_rn(tot);
       if (lane == 0) scl[t - 1] = tot;
     }
-    if (lane == 0) shf[t] = PRE ? Emb[t] : m;
+    // (PRE: the row maxima are read once at the end, not per frame — a global
+    // load feeding a store here would stall the warp every frame)
+    if constexpr (!PRE) {
+      if (lane == 0) shf[t] = m;
+    }
     // normalised alpha_t -> trellis row t (posteriors of frame t in the backward)
     if (own_row) {
       float al[K];
@@ -254,9 +258,7 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
     // did not reach are still reported (forward_backward.py:184,206)
     for (int k = fail_at; k < T; ++k) {
       if (k > fail_at) {
-        if constexpr (PRE) {
-          if (lane == 0) shf[k] = Emb[k];
-        } else {
+        if constexpr (!PRE) {
           float m = -INFINITY;
           for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
           m = warp_max(m);
@@ -270,7 +272,7 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
   {
     double acc = 0.0;
     for (int k = lane; k < T; k += 32) {
-      const double v = log(double(scl[k])) + double(shf[k]);
+      const double v = log(double(scl[k])) + double(PRE ? Emb[k] : shf[k]);
       acc += v;
       if (a.scale_logs) a.scale_logs[size_t(b) * T_max + k] = v;
     }
@@ -319,7 +321,7 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
     __syncwarp();
     const float *Lt = stage(e);
     const float *al = Lt + lay.Dr + lane * K;
-    const float m = shf[e];
+    const float m = PRE ? 0.f : shf[e];
     const float q = rcp_rn(scl[t - 1]);
     float sY = 0.f;
 #pragma unroll
@@ -630,7 +632,6 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         u = rcp_rn(tot);
         if (lane == 0) scl[t - 1] = tot;
       }
-      if (lane == 0) shf[t] = Emb[t];
       if (t < h) {  // alpha_t for the backward warp's posteriors
         float al[K];
 #pragma unroll
@@ -681,17 +682,13 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       if (lane == 0) kap[0] = fail_at < 0 ? double(scl[T - 1]) : 1.0;
       pair_sync();
     }
-    if (fail_at >= 0) {
-      for (int k = fail_at + 1; k < T; ++k)
-        if (lane == 0) shf[k] = Emb[k];
-      if (lane == 0)
-        for (int k = fail_at; k < T; ++k) scl[k] = 1.f;
-    }
+    if (fail_at >= 0 && lane == 0)
+      for (int k = fail_at; k < T; ++k) scl[k] = 1.f;
     pair_sync();  // end: the backward warp's posterior rows are written
     {
       double acc = 0.0;
       for (int k = lane; k < T; k += 32) {
-        const double val = log(double(scl[k])) + double(shf[k]);
+        const double val = log(double(scl[k])) + double(Emb[k]);
         acc += val;
         if (a.scale_logs) a.scale_logs[size_t(b) * T_max + k] = val;
       }
