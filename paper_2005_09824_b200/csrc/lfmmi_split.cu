@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kNT, 1)
           const float v = src[d];
           for (int c = 0; c < a.rep_e; ++c) dst[c * a.e_stride + d] = v;
         }
-        if (record_shift && ctid == 0) shifts[t] = Emb[t];
+        (void)record_shift;  // row maxima read once at the end (no per-frame global load)
         return;
       }
       const float *mp = mpart + (t & 1) * 32;
@@ -510,9 +510,7 @@ __global__ void __launch_bounds__(kNT, 1)
       if (fail_at >= 0) {
         // remaining shifts are row maxima, remaining scales 1 (forward_backward.py:184,206)
         for (int k = fail_at + 1 + warp; k < T; k += kNW) {
-          if (pre) {
-            if (lane == 0) shifts[k] = Emb[k];
-          } else {
+          if (!pre) {
             float m = -INFINITY;
             for (int d = lane; d < D; d += 32) m = nan_max(m, Lb[size_t(k) * D + d]);
             m = warp_max(m);
@@ -525,7 +523,7 @@ __global__ void __launch_bounds__(kNT, 1)
       {
         double acc = 0.0;
         for (int k = tid; k < T; k += kNT) {
-          const double v = log(double(scales[k])) + double(shifts[k]);
+          const double v = log(double(scales[k])) + double(pre ? Emb[k] : shifts[k]);
           acc += v;
           if (a.scale_logs) a.scale_logs[size_t(b) * a.T_max + k] = v;
         }
