@@ -431,7 +431,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   const int D = a.D, T_max = a.T_max;
   float *scl = lsm;                 // forward scales (tot of column t+1 at [t])
   float *shf = lsm + lay.T4;        // row maxima
-  float *invs = lsm + 2 * lay.T4;   // backward normalisers inv_t at [t]
+  float *invs = lsm + 2 * lay.T4;   // backward normalisers n_t = 1 / inv_t at [t]
   float *Bh = invs + lay.T4 + 4;    // backward column B_h at the midpoint
   unsigned *hist = reinterpret_cast<unsigned *>(Bh + lay.SK) + wrole * lay.Dr;
   float *ring = reinterpret_cast<float *>(Bh + lay.SK + 2 * lay.Dr) + wrole * kRing * lay.Dr;
@@ -639,8 +639,10 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         store_row_k(t, al);
       }
       if (t >= h && !other_failed) {  // posteriors of frame t: terms / Z_t, Z_t = kappa_t / scale_{t-1}
-        const double zt = kappa / double(tot);
-        const float zs = (zt > 0.0 && zt < 1e38) ? float(1.0 / zt) : 0.f;
+        // (no double divisions on the frame's path: u = 1 / scale_{t-1} and the
+        // backward normaliser n_{t+1} = 1 / inv_{t+1} are at hand)
+        const double zt = kappa * double(u);
+        const float zs = (zt > 1e-37 && zt < 1e37) ? __frcp_rn(float(zt)) : 0.f;
         const float vprev = (lane * K > 0 && lane * K - 1 < S) ? v : 0.f;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -654,7 +656,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         __syncwarp();
         flush(t);
         __syncwarp();
-        kappa = zt / double(invs[t + 1]);  // kappa_{t+1} = Z_t / inv_{t+1}
+        kappa = zt * double(invs[t + 1]);  // kappa_{t+1} = Z_t / inv_{t+1} (invs holds n = 1 / inv)
         if (t + 1 < T) load_row_k(t + 1, bcur);
       }
 #pragma unroll
@@ -761,7 +763,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       const float ld = (t < T && leak > 0.f) ? leak * sY / float(S) : 0.f;
       const float n = sY + ld * float(S);
       const float inv = (n > 0.f && n < INFINITY) ? rcp_rn(n) : 1.f;
-      if (lane == 0) invs[t] = inv;
+      if (lane == 0) invs[t] = (n > 0.f && n < INFINITY) ? n : 1.f;  // n_t = 1 / inv_t
       if (!post) {  // beta'_t = B_t inv_t -> row e (the forward warp's posteriors)
         if (t > h) {
           float bb[K];
@@ -770,7 +772,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
           store_row_k(e, bb);
         }
       } else {  // posteriors of frame e: alpha_e p e B_t / kappa_t
-        const float zinv = (kappa > 0.0 && kappa < 1e38) ? float(1.0 / kappa) : 0.f;
+        const float zinv = (kappa > 1e-37 && kappa < 1e37) ? __frcp_rn(float(kappa)) : 0.f;
         const bool nvalid = lane * K + K < S;  // state lane K + K exists
 #pragma unroll
         for (int k = 0; k < K; ++k) {
