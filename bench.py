@@ -149,7 +149,7 @@ def cpu_reference_run(w, steps, warmup, sample_b=None):
     if sample_b is not None:
         idx = list(range(min(sample_b, len(w.seqs))))
         w = type(w)(w.name, w.seed, w.S, w.I, w.D, w.lengths[idx], [w.seqs[i] for i in idx],
-                    w.den, [w.num_phones[i] for i in idx])
+                    w.den, [w.num_phones[i] for i in idx], w.lm)
     frames = w.total_frames
     if C is not None:
         import numba
@@ -223,7 +223,7 @@ def nccl_summary():
 def subset(w, idx):
     idx = [int(i) for i in idx]
     return type(w)(w.name, w.seed, w.S, w.I, w.D, np.asarray(w.lengths)[idx],
-                   [w.seqs[i] for i in idx], w.den, [w.num_phones[i] for i in idx])
+                   [w.seqs[i] for i in idx], w.den, [w.num_phones[i] for i in idx], w.lm)
 
 
 def rank_workload(args, rank, world):
@@ -348,7 +348,7 @@ def fresh_numerator_leg(P, args, w, den, dev, stream, pg, frames_all, frames_loc
                                batch_size=B * n_win)
     graphs = []
     for ph in pool.num_phones:  # graph construction: data-loader work, outside the timing
-        arcs, n, fin = synth.numerator_arcs(ph, pool.D // 2)
+        arcs, n, fin = synth.numerator_arcs(ph, pool.D // 2, lm=pool.lm)
         graphs.append(P.ChainGraph(arcs, n, pool.D, 0, fin))
     lens = np.asarray(pool.lengths, dtype=np.int64)
     offs = np.concatenate([[0], np.cumsum(lens)])

@@ -6,7 +6,7 @@ timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "s
 timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
 : > gpurun_out/configs.log
-for c in toy wsj_biphone large sweep; do
+for c in toy hmm wsj_biphone large sweep; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-extra-e2e > gpurun_out/bench_$c.log 2>&1; echo "$c rc=$?" >> gpurun_out/configs.log
   timeout 600 python bench.py --config $c --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$c.log 2>&1; echo "$c ref rc=$?" >> gpurun_out/configs.log
 done

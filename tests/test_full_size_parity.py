@@ -35,7 +35,8 @@ def _subset(w, batch, n, seed):
     return sorted(pick)
 
 
-@pytest.mark.parametrize("config,B", [("wsj_biphone", 128), ("large", 64), ("sweep", 1024)])
+@pytest.mark.parametrize("config,B", [("wsj_biphone", 128), ("large", 64), ("sweep", 1024),
+                                      ("hmm", 128)])
 def test_full_batch_vs_oracle_subset(cuda, config, B):
     import torch
 
@@ -50,7 +51,7 @@ def test_full_batch_vs_oracle_subset(cuda, config, B):
     den_kernel = str(P._backend.ext().last_den_kernel())
     torch.cuda.synchronize()
     assert int(round(float(tot[2]))) == 0
-    idx = _subset(w, batch, 32, seed={"wsj_biphone": 1, "large": 2, "sweep": 3}[config])
+    idx = _subset(w, batch, 32, seed={"wsj_biphone": 1, "large": 2, "sweep": 3, "hmm": 4}[config])
     sub = P.make_batch([batch.values[b, :batch.lengths[b]] for b in idx])
     sub_nums = [nums.graph(b) for b in idx]
     sub_nums = P.ChainGraphBatch.from_graphs([sub_nums[j] for j in sub.order_map])

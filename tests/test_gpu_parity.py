@@ -136,7 +136,7 @@ def _kernel_env(kernel, lib_options):
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "noring",
                                     "group"])
-@pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None),
+@pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None), ("hmm", 24),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])
 def test_configs_vs_oracle(cuda, config, batch_size, kernel, lib_options):
