@@ -276,12 +276,12 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
   }
   if (work_bytes < size_t(a.S_pad) * sizeof(Real))
     return set_error(LFMMI_ERR_INVALID, "workspace too small");
-  // Numerator-sized graphs: one warp per utterance.  Larger graphs: one CTA
-  // per utterance with the arc layout in shared memory.  The choice depends
-  // only on the graph batch, so an utterance's result never depends on which
-  // other utterances share its batch.
-  const bool small = graphs->max_states <= 512;
+  // Numerator-sized graphs: a warp group per utterance.  Larger or denser
+  // graphs (a 43-state phone-bigram den has ~1850 arcs): the den kernels.  The
+  // choice depends only on the graph batch, so an utterance's result never
+  // depends on which other utterances share its batch.
   const Options &opt = options();
+  const bool small = graphs->max_states <= 512 && graphs->max_arcs <= opt.small_arcs;
   if constexpr (std::is_same<Real, float>::value) {
     if (graphs->linear && opt.linear) {  // the reference's numerators: linear chains
       const int rc = launch_linear(a, graphs, st);
@@ -618,11 +618,12 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
                                  num_log_probs, num_fail, nullptr, s, packed, E, Em);
   };
   auto den_pass = [&]() {
-    return forward_backward_impl(denominator, den_row_map, batch, max_frames, num_pdfs, precision,
-                                 loglikes, lengths, leak, scale_floor, den_leak_pi, total_frames,
-                                 ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE, nullptr,
-                                 den_log_probs, den_fail, nullptr, stream, packed, E, Em,
-                                 num_reserve);
+    const int rc = forward_backward_impl(
+        denominator, den_row_map, batch, max_frames, num_pdfs, precision, loglikes, lengths, leak,
+        scale_floor, den_leak_pi, total_frames, ws + den_off, den_bytes, grad, LFMMI_POST_NEGATE,
+        nullptr, den_log_probs, den_fail, nullptr, stream, packed, E, Em, num_reserve);
+    note_den_kernel(g_kernel);  // whichever family the denominator took (incl. small dens)
+    return rc;
   };
   if (serial) {
     rc = num_pass(st);

@@ -29,6 +29,7 @@ const Field kFields[] = {
     {"stream_mode", nullptr, &Options::stream_mode},
     {"stream_ring", &Options::stream_ring, nullptr},
     {"num_group", &Options::num_group, nullptr},
+    {"small_arcs", &Options::small_arcs, nullptr},
     {"tile_xdb", &Options::tile_xdb, nullptr},
     {"serial", &Options::serial, nullptr},
     {"emit", &Options::emit, nullptr},

@@ -21,6 +21,8 @@ struct Options {
   std::string stream_mode = "auto";  // "auto" | "1024x1" | "1024x2" | "512x2"
   int stream_ring = 1;    // stream kernel: TMA slot ring when it fits (biphone 9.45 vs 9.96 ms)
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
+  int small_arcs = 1024;  // graphs with <= 512 states AND <= this many arcs per row take the
+                          // numerator-sized kernels; denser ones (a phone-bigram den) the den path
   int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots
   int serial = 0;         // chain_loss: numerator pass before the den pass (-1 auto: B > 2 x SMs)
   int emit = 1;           // chain_loss (fp32): emissions pre-pass shared by the passes

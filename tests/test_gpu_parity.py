@@ -120,7 +120,8 @@ def _kernel_env(kernel, lib_options):
     """Kernel selection shared by the parity tests: denominator "tile" (one CTA
     per utterance), "split1"/"split2" (2-CTA split, 1 or 2 clusters), "tile1x"
     (tile kernel with one posterior slot buffer), "numtile" (numerators through
-    the generic tile kernel instead of the linear-chain kernel)."""
+    the generic tile kernel instead of the linear-chain kernel), "smallnum" /
+    "smallden" (the small-graph threshold moved either way)."""
     if kernel == "tile":  # one CTA per utterance (no forward/backward split)
         lib_options(split=0)
     if kernel in ("split1", "split2"):  # 2-CTA split, several utterances per cluster
@@ -132,10 +133,14 @@ def _kernel_env(kernel, lib_options):
         lib_options(linear=0)
     if kernel == "noring":  # stream kernel reading slot rows straight from L2 (no TMA ring)
         lib_options(stream_ring=0, stream_mode="1024x1")
+    if kernel == "smallnum":  # every graph <= 512 states (the hmm den too) numerator-sized
+        lib_options(small_arcs=1 << 30)
+    if kernel == "smallden":  # every graph on the den kernels (numerators too)
+        lib_options(small_arcs=0, linear=0)
 
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "noring",
-                                    "group"])
+                                    "group", "smallnum", "smallden"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None), ("hmm", 24),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])
