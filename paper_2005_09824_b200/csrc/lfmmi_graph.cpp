@@ -390,6 +390,8 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
 
     // ---- tile packs (scheduled, 16-bit state / pdf / posterior-slot encoding) ----
     bool tileable = S <= 16383 && num_pdfs <= 16383 && I <= 65535 && mi < 65536 && mo < 65536;
+    d[kTileG] = 1;
+    d[kNTiles] = 0;
     d[kTileOff] = int(h.tf_trips.size());
     d[kTfSlotOff] = int(h.tf_word.size());
     d[kTbSlotOff] = int(h.tb_word.size());
@@ -398,10 +400,14 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
       const size_t a0 = size_t(d[kArcOff]);
       const int *iptr = &h.in_ptr[h.in_ptr.size() - (S + 1)];
       const int *optr = &h.out_ptr[h.out_ptr.size() - (S + 1)];
+      // small dense graphs: a state's arc list over G adjacent lanes (both packs)
+      const int G = tile_lanes_per_state(S, std::max(mi, mo), options().tile_g);
       TileSchedule tf = schedule_tiles(S, iptr, &h.in_src[a0], &h.in_pdf[a0], &h.in_p64[a0], gl,
-                                       true);
+                                       true, -1, G);
       TileSchedule tb = schedule_tiles(S, optr, &h.out_dst[a0], &h.out_pdf[a0], &h.out_p64[a0],
-                                       gl, true);
+                                       gl, true, -1, G);
+      d[kTileG] = G;
+      d[kNTiles] = int(tf.trips.size());
       std::vector<int> pptr, xslot;
       int xpad = 0;
       assign_xslots(tb, &h.out_pdf[a0], num_pdfs, I, 4, pptr, xslot, xpad);

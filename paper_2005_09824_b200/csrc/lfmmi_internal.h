@@ -25,7 +25,7 @@ enum DescField : int {
   kMaxOutDeg = 10,
   // tile packs (fb_tile_kernel): states sorted by degree into 32-lane tiles,
   // arc slots stored slot-major per tile (slot j of lane l at base + 32 j + l)
-  kTileOff = 11,     // offset into per-tile arrays (trips/base), tiles = ceil(S/32)
+  kTileOff = 11,     // offset into per-tile arrays (trips/base), kNTiles tiles
   kTfSlotOff = 12,   // forward (by destination) slot offset
   kTfSlots = 13,     // forward slot count (multiple of 32)
   kTbSlotOff = 14,   // backward (by source) slot offset
@@ -40,7 +40,10 @@ enum DescField : int {
   kSTiles = 21,      // tiles per phase (0 = no stream pack for this row)
   kSfSlotOff = 22,   // forward (by destination) slot offset
   kSbSlotOff = 23,   // backward (by source) slot offset
-  kDescInts = 24
+  kNTiles = 24,      // tile packs: tiles per phase = ceil(S * kTileG / 32)
+  kTileG = 25,       // tile packs: lanes per state (power of 2; a state's arcs split
+                     // over G adjacent lanes, summed with xor shuffles; 1 = one lane)
+  kDescInts = 26
 };
 
 // Device-side view of a packed graph batch (passed by value to kernels).

@@ -430,8 +430,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   const int lane = threadIdx.x & 31, wrole = threadIdx.x >> 5;  // 0 forward, 1 backward
   const int D = a.D, T_max = a.T_max;
   float *scl = lsm;                 // forward scales (tot of column t+1 at [t])
-  float *shf = lsm + lay.T4;        // row maxima
-  float *invs = lsm + 2 * lay.T4;   // backward normalisers n_t = 1 / inv_t at [t]
+  float *invs = lsm + 2 * lay.T4;   // (lsm + T4: row maxima slot, unused with E rows)   // backward normalisers n_t = 1 / inv_t at [t]
   float *Bh = invs + lay.T4 + 4;    // backward column B_h at the midpoint
   unsigned *hist = reinterpret_cast<unsigned *>(Bh + lay.SK) + wrole * lay.Dr;
   float *ring = reinterpret_cast<float *>(Bh + lay.SK + 2 * lay.Dr) + wrole * kRing * lay.Dr;

@@ -35,6 +35,7 @@ const Field kFields[] = {
     {"emit", &Options::emit, nullptr},
     {"sched_iters", &Options::sched_iters, nullptr},
     {"chore_bias", &Options::chore_bias, nullptr},
+    {"tile_g", &Options::tile_g, nullptr},
     {"debug", &Options::debug, nullptr},
     {"profile", nullptr, &Options::profile},
 };

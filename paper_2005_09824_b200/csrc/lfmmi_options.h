@@ -28,6 +28,7 @@ struct Options {
   int emit = 1;           // chain_loss (fp32): emissions pre-pass shared by the passes
   int sched_iters = -1;   // bank-conflict local search moves per slot row (-1 auto)
   int chore_bias = 16;    // den warp lists: extra slot rows charged to the chore warps (pack time)
+  int tile_g = 0;         // tile packs: lanes per state (0 auto, else forced power of 2; pack time)
   int debug = 0;          // layout / dispatch notes on stderr
   std::string profile;    // "" | "split" | "tile": per-frame cycle counters on stderr
 };

@@ -182,10 +182,22 @@ RowEval eval_row(const int *arcs, const int *gidx, const int *pdf, const GatherL
 
 }  // namespace
 
+int tile_lanes_per_state(int S, int max_deg, int force) {
+  if (force > 0) {
+    int g = 1;
+    while (g < 32 && g * 2 <= force) g *= 2;
+    return g;
+  }
+  int g = 1;
+  while (g < 32 && S * g * 2 <= 512 && max_deg >= 8 * g) g *= 2;
+  return g;
+}
+
 TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
                             const double *prob, const GatherLayout &gl, bool optimize,
-                            int iters_per_row) {
+                            int iters_per_row, int lanes_per_state) {
   const int ls_iters = iters_per_row >= 0 ? iters_per_row : local_search_iters(S);
+  const int G = lanes_per_state;
   std::vector<int> sorted(S);
   std::iota(sorted.begin(), sorted.end(), 0);
   std::stable_sort(sorted.begin(), sorted.end(), [&](int x, int y) {
@@ -199,7 +211,7 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
   // residue the tile does not hold yet, when one exists.
   std::vector<int> order;
   order.reserve(S);
-  if (optimize) {
+  if (optimize && G == 1) {
     // per degree: pool of states bucketed by residue
     std::vector<int> deg_of(S);
     int maxdeg = 0;
@@ -230,7 +242,7 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
   } else {
     order = sorted;
   }
-  const int ntiles = (S + 31) / 32;
+  const int ntiles = (S * G + 31) / 32;
   // Tiles are independent: schedule them in parallel into per-tile fragments
   // (each with its own RNG seed, so the result does not depend on threading).
   auto do_tile = [&](int w, TileSchedule &ts) {
@@ -239,15 +251,15 @@ TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *p
     std::vector<std::vector<int>> rem(32);
     int trips = 0;
     for (int l = 0; l < 32; ++l) {
-      const int k = 32 * w + l;
+      const int k = (32 * w + l) / G, sub = (32 * w + l) % G;
       if (k >= S) {
         ts.info.push_back(0xFFFFu);
         continue;
       }
       const int s = order[k];
-      const int deg = ptr[s + 1] - ptr[s];
+      for (int a = ptr[s] + sub; a < ptr[s + 1]; a += G) rem[l].push_back(a);
+      const int deg = int(rem[l].size());
       ts.info.push_back(unsigned(s) | (unsigned(deg) << 16));
-      for (int a = ptr[s]; a < ptr[s + 1]; ++a) rem[l].push_back(a);
       trips = std::max(trips, deg);
     }
     ts.trips.push_back(trips);

@@ -25,9 +25,18 @@ struct TileSchedule {
 
 // ptr: CSR row pointers (S + 1) of the layout; gidx/pdf/prob per CSR arc.
 // iters_per_row < 0: the default local-search budget (option sched_iters / auto).
+// lanes_per_state G (power of 2 <= 32): state k of the degree order owns lanes
+// [kG, kG + G) of the lane sequence, lane j of them the arcs j, j + G, ... of
+// its CSR row; tiles = ceil(S G / 32).  G > 1 splits the long in/out lists of a
+// small dense graph (a phone-bigram den: 43 states, ~44 arcs each) over lanes.
 TileSchedule schedule_tiles(int S, const int *ptr, const int *gidx, const int *pdf,
                             const double *prob, const GatherLayout &gl, bool optimize,
-                            int iters_per_row = -1);
+                            int iters_per_row = -1, int lanes_per_state = 1);
+
+// Lanes per state of a row's tile packs: the largest power of 2 with at most
+// 512 lanes in all (one 16-warp CTA) and >= 4 arcs per lane on the longest
+// list; 1 for every graph with more than 256 states.  force > 0 overrides.
+int tile_lanes_per_state(int S, int max_deg, int force);
 
 // Posterior slot of every backward tile slot: pdf groups (16-byte aligned,
 // `slack` spare positions each), conflict-avoiding positions per slot row,

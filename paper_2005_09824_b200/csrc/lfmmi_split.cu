@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kNT, 1)
   auto bind = [&](int row) {
     const int *desc = a.g.desc + row * kDescInts;
     const int so = desc[fwd ? kTfSlotOff : kTbSlotOff], nsl = desc[fwd ? kTfSlots : kTbSlots];
-    const int ntiles = (desc[kS] + 31) / 32, toff = desc[kTileOff];
+    const int ntiles = desc[kNTiles], toff = desc[kTileOff];
     copy16<kNT>(smem + lay.wp, (fwd ? a.g.tf_wp : a.g.tb_wp) + so, size_t(nsl) * 8, tid);
     copy16<kNT>(smem + lay.xs, (fwd ? a.g.tf_xslot : a.g.tb_xslot) + so, size_t(nsl) * 2, tid);
     copy16<kNT>(smem + lay.tinfo, (fwd ? a.g.tf_info : a.g.tb_info) + size_t(toff) * 32,
@@ -239,6 +239,8 @@ __global__ void __launch_bounds__(kNT, 1)
     const int row = int(a.row_map[b]);
     const int *desc = a.g.desc + row * kDescInts;
     const int S = desc[kS], init = desc[kInit];
+    const int G = desc[kTileG];  // lanes per state: partial sums over G adjacent lanes
+    const bool lead = (lane & (G - 1)) == 0;
     const float *fin = a.g.fin32 + desc[kStateOff];
     const float upi = float(1.0 / double(S));
     // forward CTA: posteriors of frames >= h; backward CTA: < h.  The forward
@@ -451,7 +453,8 @@ __global__ void __launch_bounds__(kNT, 1)
                 fwd_tile_f32<false>(wp32 + uint32_t(base) * 8u, trips, e32, r32, A, Bs);
               raw = inv2 * (A + lu * Bs);
             }
-            if (s != 0xFFFF) {
+            raw = group_sum(raw, G);
+            if (s != 0xFFFF && lead) {
               if (last) raw *= fin[s];
               put_vec(rn, s, raw);
               psum += raw;
@@ -616,7 +619,8 @@ __global__ void __launch_bounds__(kNT, 1)
               } else {
                 A = bwd_plain_tile_f32(wp32 + uint32_t(base) * 8u, trips, e32, b32, ld);
               }
-              if (s != 0xFFFF) {
+              A = group_sum(A, G);
+              if (s != 0xFFFF && lead) {
                 const float v = inv * A;
                 put_vec(bn, s, v);
                 dq = fmaf(upi, v, dq);

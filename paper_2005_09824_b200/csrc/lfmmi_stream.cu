@@ -43,7 +43,6 @@ namespace lfmmi {
 
 namespace {
 
-constexpr int kStreamThreads = 1024;
 constexpr int kMaxD = 2048;  // log-likelihood row held in registers: kMaxD / NT per thread
 constexpr float kPostScale = 268435456.f;  // 2^28: posterior bins in uint32 fixed point
 constexpr int kRingRows = 8;               // slot rows per TMA chunk (8 x 256 B = 2 KB)

@@ -171,7 +171,9 @@ __global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks 
   const int row = int(a.row_map[b]);
   const int *desc = a.g.desc + row * kDescInts;
   const int S = desc[kS], init = desc[kInit];
-  const int ntiles = (S + 31) / 32;
+  const int ntiles = desc[kNTiles];
+  const int G = desc[kTileG];  // lanes per state: partial sums over G adjacent lanes
+  const bool lead = (lane & (G - 1)) == 0;
   const int toff = desc[kTileOff];
   const Real *fin = pick<Real>(a.g.fin32, a.g.fin64) + desc[kStateOff];
   const Real *Lb = a.L + size_t(b) * a.T_max * D;
@@ -452,7 +454,9 @@ __global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks 
           }
         }
         const int s = int(info & 0xFFFFu);
-        if (s != 0xFFFF) {
+        A = group_sum(A, G);
+        Bs = group_sum(Bs, G);
+        if (s != 0xFFFF && lead) {
           Real raw = inv2 * (A + leakc * (CUSTOM_PI ? Bs : upi * Bs));
           if (last) raw *= fin[s];
           put_vec(rn, s, raw);
@@ -629,7 +633,8 @@ __global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks 
             xt[XS[base + 32 * j]] = as * term;
           }
         }
-        if (s != 0xFFFF) {
+        A = group_sum(A, G);
+        if (s != 0xFFFF && lead) {
           const Real v = inv * A;
           put_vec(bn, s, v);
           dp = fma(CUSTOM_PI ? pi[s] : upi, v, dp);

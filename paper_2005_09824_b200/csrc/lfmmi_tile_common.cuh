@@ -58,6 +58,14 @@ __device__ __forceinline__ Real lane_sum(const Real *v, int lane) {
   }
 }
 
+// Sum over the G (power of 2) adjacent lanes that share one state of a tile
+// pack (kTileG); every lane of the group gets the same value.
+template <typename Real>
+__device__ __forceinline__ Real group_sum(Real v, int G) {
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
 struct SlotF32 {
   const uint2 *wp;
   __device__ __forceinline__ void load(int slot, unsigned &w, float &p) const {

@@ -121,7 +121,8 @@ def _kernel_env(kernel, lib_options):
     per utterance), "split1"/"split2" (2-CTA split, 1 or 2 clusters), "tile1x"
     (tile kernel with one posterior slot buffer), "numtile" (numerators through
     the generic tile kernel instead of the linear-chain kernel), "smallnum" /
-    "smallden" (the small-graph threshold moved either way)."""
+    "smallden" (the small-graph threshold moved either way), "g2" / "g4s" (tile
+    packs with 2 / 4 lanes per state on the tile / split kernels)."""
     if kernel == "tile":  # one CTA per utterance (no forward/backward split)
         lib_options(split=0)
     if kernel in ("split1", "split2"):  # 2-CTA split, several utterances per cluster
@@ -137,10 +138,14 @@ def _kernel_env(kernel, lib_options):
         lib_options(small_arcs=1 << 30)
     if kernel == "smallden":  # every graph on the den kernels (numerators too)
         lib_options(small_arcs=0, linear=0)
+    if kernel == "g2":  # tile packs with two lanes per state (pack time), tile kernel
+        lib_options(tile_g=2, split=0)
+    if kernel == "g4s":  # four lanes per state, split kernel
+        lib_options(tile_g=4, split=1)
 
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "noring",
-                                    "group", "smallnum", "smallden"])
+                                    "group", "smallnum", "smallden", "g2", "g4s"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None), ("hmm", 24),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])
