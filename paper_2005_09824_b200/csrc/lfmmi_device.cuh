@@ -126,6 +126,39 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// The same on 32-bit shared-window addresses (no generic -> shared conversion).
+__device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void *src, unsigned bytes,
+                                              uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// 32-bit shared-memory integer reduction (RED, no return value).
+__device__ __forceinline__ void red_add_shared(uint32_t addr, unsigned v) {
+  asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(addr), "r"(v));
+}
+// ... skipped (predicated, no branch) when v == 0.
+__device__ __forceinline__ void red_add_shared_nz(uint32_t addr, unsigned v) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p red.shared.add.u32 [%0], %1;\n}\n" ::"r"(
+          addr),
+      "r"(v));
+}
 
 __host__ __device__ inline int pad4(int x) { return (x + 3) & ~3; }
 

@@ -31,6 +31,8 @@
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
 #include "lfmmi_options.h"
+#include "lfmmi_ring.cuh"
+#include "lfmmi_tile_common.cuh"
 
 #include <cooperative_groups.h>
 
@@ -217,85 +219,26 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     my_base = lane < ntw ? __ldg(base_arr + tl) : 0;
   };
 
-  // ---- TMA slot ring (RING) ---------------------------------------------------------
-  // Every frame re-reads the same slot rows, so each warp streams its tiles' rows
-  // into a private ring of nslot chunks (kRingRows x 256 B, cp.async.bulk
-  // completing on one mbarrier per slot) that runs nslot chunks ahead of the
-  // arc loop — across tile and frame boundaries — instead of a dependent L2
-  // load per row.  Counters are absolute (never reset), so slot = g % nslot
-  // and the wait parity is (g / nslot) & 1 across both phases.
-  uint2 *ring = reinterpret_cast<uint2 *>(smem + lay.ring);
-  unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
-  constexpr int nslot = kRingSlots;  // compile-time: slot = g & 1, parity = (g >> 1) & 1
-  unsigned g_cons = 0, g_iss = 0, g_end = 0;  // chunks consumed / issued / phase end
-  int p_i = 0;                                // producer cursor: chunk of this warp's table
-  const uint2 *pack = nullptr;
-  auto slot_ptr = [&](unsigned g) { return ring + (size_t(warp) * nslot + g % nslot) * (kRingRows * 32); };
-  auto slot_bar = [&](unsigned g) { return bars + warp * nslot + g % nslot; };
-  // This warp's chunks of one frame, in consumption order, as {slot offset into
-  // the pack, bytes} — built once per phase so the producer (lane 0) is a table
-  // read plus the bulk copy.
-  uint2 *ctab = reinterpret_cast<uint2 *>(smem + lay.ctab) + size_t(warp) * kRingChunks;
-  int nchunk = 0;
-  auto issue = [&]() {
-    if (lane == 0) {
-      const uint2 ent = ctab[p_i];
-      fence_proxy_async_smem();
-      bulk_copy_g2s(slot_ptr(g_iss), pack + ent.x, ent.y, slot_bar(g_iss));
-    }
-    ++g_iss;
-    if (++p_i == nchunk) p_i = 0;
-  };
+  // ---- TMA slot ring (RING): lfmmi_ring.cuh ---------------------------------------
+  SlotRing<kRingSlots, kRingRows, kRingChunks> ring;
   auto begin_phase = [&](const uint2 *pk, int frames) {
-    if constexpr (RING) {
-      pack = pk;
-      p_i = 0;
-      int c = 0;
-      for (int i = 0; i < ntw; ++i) {
-        const int tr = __shfl_sync(kFull, my_trips, i);
-        const int bs = __shfl_sync(kFull, my_base, i);
-        for (int j0 = 0; j0 < tr; j0 += kRingRows, ++c)
-          if (lane == 0 && c < kRingChunks)
-            ctab[c] = make_uint2(unsigned(bs + 32 * j0), unsigned(min(kRingRows, tr - j0)) * 256u);
-      }
-      nchunk = c;  // (the launcher guarantees c <= kRingChunks)
-      __syncwarp();
-      g_end = g_iss + unsigned(c) * unsigned(frames);
-      for (int q = 0; q < nslot && g_iss < g_end; ++q) issue();
-    }
+    if constexpr (RING) ring.begin(pk, ntw, my_trips, my_base, frames);
   };
   auto drain = [&]() {  // wait for copies still in flight (early exit of a phase)
-    if constexpr (RING) {
-      for (; g_cons < g_iss; ++g_cons) mbar_wait(slot_bar(g_cons), (g_cons / nslot) & 1u);
-      __syncwarp();
-    }
+    if constexpr (RING) ring.drain();
   };
   // Arc rows [0, trips) of one tile: body(w) per slot word (this lane's arc).
   auto tile_rows = [&](const uint2 *sp, int trips, auto &&body) {
     if constexpr (RING) {
-      for (int j0 = 0; j0 < trips; j0 += kRingRows) {
-        mbar_wait(slot_bar(g_cons), (g_cons / nslot) & 1u);
-        const uint2 *sl = slot_ptr(g_cons) + lane;
-        const int n = min(kRingRows, trips - j0);
-        uint2 w[kRingRows];
-#pragma unroll
-        for (int r = 0; r < kRingRows; ++r)
-          if (r < n) w[r] = sl[32 * r];
-        __syncwarp();  // every lane has its words: the slot may be refilled
-        ++g_cons;
-        if (g_iss < g_end) issue();
-#pragma unroll
-        for (int r = 0; r < kRingRows; ++r)
-          if (r < n) body(w[r]);
-      }
+      ring.rows(trips, body);
     } else {
 #pragma unroll 8
       for (int j = 0; j < trips; ++j) body(ldg_slot(sp + 32 * j));
     }
   };
   if constexpr (RING) {
-    if (tid < NW * nslot) mbar_init(bars + tid, 1);
-    mbar_init_fence();
+    ring.init(smem + lay.ring, smem + lay.bars, smem + lay.ctab, warp, lane);
+    decltype(ring)::init_barriers(smem + lay.bars, NW, tid);
     gsync();
   }
 
@@ -350,8 +293,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     for (int j = 0; j < kEPT; ++j) rn[j] = rn2[j];
     load_row(k + 3, rn2);
     {
-      const float *e = ebuf + cur * D_pad;
-      const float *r = vec + cur * S32;
+      const uint32_t e32 = smem_u32(ebuf + cur * D_pad), r32 = smem_u32(vec + cur * S32);
       float *rnew = vec + nxt * S32, *rnew_p = vec_p + nxt * S32;
       const bool last = (k + 1 == T);
       float psum = 0.f;
@@ -364,8 +306,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
         const uint2 *sp = fwp + __shfl_sync(kFull, my_base, i) + lane;
         float A = 0.f, Bs = 0.f;
         tile_rows(sp, trips, [&](const uint2 w) {
-          const float q = __uint_as_float(w.y) * e[w.x >> 15];
-          A = fmaf(q, r[w.x & 0x7FFFu], A);
+          const float q = __uint_as_float(w.y) * lds_f(e32 + ((w.x >> 15) << 2));
+          A = fmaf(q, lds_f(r32 + ((w.x & 0x7FFFu) << 2)), A);
           Bs += q;
         });
         if (s >= 0) {
@@ -465,11 +407,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     for (int j = 0; j < kEPT; ++j) rn[j] = rn2[j];
     load_row(t - 4, rn2);
     {
-      const float *bt = vec + ct * S32;
+      const uint32_t b32 = smem_u32(vec + ct * S32), e32 = smem_u32(ebuf + cp * D_pad);
       float *bnew = vec + cp * S32, *bnew_p = vec_p + cp * S32;
-      const float *e = ebuf + cp * D_pad;
       const float *arow = trellis + size_t(t - 1) * S32;  // alpha_{t-1}, backward-pack order
-      unsigned *bn = bins + cp * D_pad;
+      const uint32_t bn32 = smem_u32(bins + cp * D_pad);
       float dp = 0.f;
       int s_next = -1;
       float a_next = 0.f;
@@ -490,11 +431,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
         float A = 0.f;
         tile_rows(sp, trips, [&](const uint2 w) {
           const float pr = __uint_as_float(w.y);
-          const unsigned pdf = w.x >> 15;
-          const float term = pr * e[pdf] * (bt[w.x & 0x7FFFu] + ld);
+          const uint32_t pdf4 = (w.x >> 15) << 2;
+          const float term = pr * lds_f(e32 + pdf4) * (lds_f(b32 + ((w.x & 0x7FFFu) << 2)) + ld);
           A += term;
           const unsigned q = __float2uint_rn(as * term * kPostScale);
-          if (q) atomicAdd(bn + pdf, q);
+          red_add_shared_nz(bn32 + pdf4, q);
         });
         if (s >= 0) {
           const float v = inv * A;
@@ -559,7 +500,7 @@ static int launch_stream_impl(const FBArgs<float> &a, const lfmmi_graphs *g, int
   // per warp and frame: <= ceil(tiles / (CL NW)) tiles of <= max_deg rows
   const int tiles_per_warp = (g->max_stiles + CL * NW - 1) / (CL * NW);
   const int max_deg = std::max(g->max_in_deg, g->max_out_deg);
-  const bool fits = tiles_per_warp * ((max_deg + kRingRows - 1) / kRingRows) <= kRingChunks;
+  const bool fits = ring_chunks_needed(tiles_per_warp, max_deg, kRingRows) <= kRingChunks;
   if (options().stream_ring && fits) {
     const StreamLayout lay = stream_layout(S32, a.D_pad, a.T_pad, NW, kRingSlots);
     if (lay.total <= unsigned(kMaxSmem)) return launch_stream_impl2<NT, CL, true>(a, S32, lay, st);
@@ -585,12 +526,18 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   // Two SMs per utterance (2-CTA cluster of 1024-thread CTAs) while the batch
   // leaves SMs idle, else one 1024-thread CTA per utterance.  ("512x2" — two
   // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
-  // "split": the forward | backward split (lfmmi_streamsplit.cu; correct, but
-  // measured no faster: biphone 9.94 vs 9.96 ms, large 38.7 vs 30.1 ms — its
-  // frames are latency-bound on per-warp L2 slot loads like these, and doubling
-  // the SMs per utterance does not shorten them).
+  // "split": the forward | backward split (lfmmi_streamsplit.cu).  With the TMA
+  // slot ring it is the default once the batch fills the SMs (biphone 7.75 vs
+  // 9.09 ms for 1024x1 with its ring); reading slot rows from L2 it is not
+  // faster (biphone 9.67 ms, large 35.5 vs 30.7 ms: frames latency-bound on the
+  // per-warp slot loads), so graphs whose columns leave no room for the ring
+  // (large) stay on 1024x2 / 1024x1.
   const std::string &want = options().stream_mode;
   if (want == "split") return launch_stream_split(a, g, st);
+  if (want == "auto" && 2 * a.B > sms && options().stream_ring) {
+    const int rc = launch_stream_split(a, g, st, true);
+    if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
+  }
   std::string mode = want != "auto" ? want : (2 * a.B <= sms ? "1024x2" : "1024x1");
   if (mode == "1024x2") return launch_stream_impl<1024, 2>(a, g, S32, lay, st);
   if (mode == "512x2") return launch_stream_impl<512, 2>(a, g, S32, lay, st);

@@ -39,6 +39,8 @@
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
 #include "lfmmi_options.h"
+#include "lfmmi_ring.cuh"
+#include "lfmmi_tile_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -49,12 +51,14 @@ constexpr int kNT = 1024, kNW = kNT / 32;
 constexpr int kMaxD = 2048, kEPT = kMaxD / kNT;  // log-likelihood elements per thread
 constexpr float kPostScale = 268435456.f;        // 2^28
 constexpr int kMaxItems = 64;                    // utterances per cluster
+// TMA slot ring (as fb_stream_kernel): 2 chunks of 8 slot rows per warp
+using Ring = SlotRing<2, 8, 64>;
 
 struct SSLayout {
-  unsigned vec, ebuf, bins, scales, invs, shifts, part, mpart, misc, items, total;
+  unsigned vec, ebuf, bins, scales, invs, shifts, part, mpart, misc, items, ring, bars, ctab, total;
 };
 
-__host__ __device__ inline SSLayout ss_layout(int S32, int D_pad, int T_pad) {
+__host__ __device__ inline SSLayout ss_layout(int S32, int D_pad, int T_pad, bool ring) {
   SSLayout l;
   unsigned o = 512;  // scratch: 32 doubles + 32 int64
   auto take = [&](unsigned bytes) {
@@ -72,6 +76,9 @@ __host__ __device__ inline SSLayout ss_layout(int S32, int D_pad, int T_pad) {
   l.mpart = take(2u * 32u * 4u);
   l.misc = take(64u);  // [0] kappa_h (double), [8] ld_h (float), [12] fail flag (int)
   l.items = take(unsigned(kMaxItems + 4) * 4u);
+  l.ring = take(ring ? Ring::slot_bytes(kNW) : 0u);
+  l.bars = take(ring ? Ring::bar_bytes(kNW) : 0u);
+  l.ctab = take(ring ? Ring::table_bytes(kNW) : 0u);
   l.total = o;
   return l;
 }
@@ -91,6 +98,7 @@ __device__ __forceinline__ void cluster_sync_rows() {
 
 }  // namespace
 
+template <bool RING>
 __global__ void __launch_bounds__(kNT, 1)
     fb_streamsplit_kernel(const FBArgs<float> a, int S32, const SSLayout lay, int nclusters,
                           int hnum) {
@@ -166,6 +174,12 @@ __global__ void __launch_bounds__(kNT, 1)
     __syncthreads();
   }
   const int nitems = items[0];
+  Ring ring;
+  if constexpr (RING) {
+    ring.init(smem + lay.ring, smem + lay.bars, smem + lay.ctab, warp, lane);
+    Ring::init_barriers(smem + lay.bars, kNW, tid);
+    __syncthreads();
+  }
 
   for (int it = 0; it < nitems; ++it) {
     const int b = items[4 + it];
@@ -257,6 +271,19 @@ __global__ void __launch_bounds__(kNT, 1)
     const int my_trips = lane < ntw ? __ldg(trips_arr + warp + kNW * lane) : 0;
     const int my_base = lane < ntw ? __ldg(base_arr + warp + kNW * lane) : 0;
     for (int d = tid; d < 2 * D_pad; d += kNT) bins[d] = 0u;
+    // Arc rows of one tile: body(w) per slot word, from the ring or from L2.
+    auto tile_rows = [&](const uint2 *sp, int trips, auto &&body) {
+      if constexpr (RING) {
+        ring.rows(trips, body);
+      } else {
+#pragma unroll 8
+        for (int j = 0; j < trips; ++j) body(ldg_slot(sp + 32 * j));
+      }
+    };
+    // this CTA's arc-loop frames of the item: forward T (fewer only on a
+    // failure, which drains the ring), backward T - h (+ h posterior frames)
+    if constexpr (RING)
+      ring.begin(wp, ntw, my_trips, my_base, fwd ? T : (other_failed ? T - h : T));
 
     if (fwd) {
       // ======================= forward CTA ==============================================
@@ -307,6 +334,7 @@ __global__ void __launch_bounds__(kNT, 1)
           }
           if (!(t2 >= a.floor_eff) || isinf(t2)) {
             fail_at = k - 1;
+            if constexpr (RING) ring.drain();
             break;
           }
           inv2 = __frcp_rn(t2);
@@ -333,11 +361,10 @@ __global__ void __launch_bounds__(kNT, 1)
         load_row(k + 3, rn2);
         if (post && k > h) flush(k - 1, (k - 1) & 1);
         {
-          const float *e = ebuf + cur * D_pad;
-          const float *r = vec + cur * S32;
+          const uint32_t e32 = smem_u32(ebuf + cur * D_pad), r32 = smem_u32(vec + cur * S32);
           float *rnew = vec + nxt * S32;
           const float *brow = trellis + size_t(k) * S32;  // beta'_{k+1} (forward-pack order)
-          unsigned *bn = bins + cur * D_pad;
+          const uint32_t bn32 = smem_u32(bins + cur * D_pad);
           const bool last = (k + 1 == T);
           float psum = 0.f;
           int s_next = ntw > 0 ? __ldg(finfo + warp * 32 + lane) : -1;
@@ -354,25 +381,20 @@ __global__ void __launch_bounds__(kNT, 1)
             const uint2 *sp = wp + __shfl_sync(kFull, my_base, i) + lane;
             float A = 0.f, Bs = 0.f;
             if (post) {
-#pragma unroll 8
-              for (int j = 0; j < trips; ++j) {
-                const uint2 w = ldg_slot(sp + 32 * j);
-                const unsigned pdf = w.x >> 15;
-                const float q = __uint_as_float(w.y) * e[pdf];
-                const float rs = r[w.x & 0x7FFFu];
+              tile_rows(sp, trips, [&](const uint2 w) {
+                const uint32_t pdf4 = (w.x >> 15) << 2;
+                const float q = __uint_as_float(w.y) * lds_f(e32 + pdf4);
+                const float rs = lds_f(r32 + ((w.x & 0x7FFFu) << 2));
                 A = fmaf(q, rs, A);
                 Bs += q;
-                const unsigned fx = __float2uint_rn(q * (rs + lu) * cb * kPostScale);
-                if (fx) atomicAdd(bn + pdf, fx);
-              }
+                red_add_shared_nz(bn32 + pdf4, __float2uint_rn(q * (rs + lu) * cb * kPostScale));
+              });
             } else {
-#pragma unroll 8
-              for (int j = 0; j < trips; ++j) {
-                const uint2 w = ldg_slot(sp + 32 * j);
-                const float q = __uint_as_float(w.y) * e[w.x >> 15];
-                A = fmaf(q, r[w.x & 0x7FFFu], A);
+              tile_rows(sp, trips, [&](const uint2 w) {
+                const float q = __uint_as_float(w.y) * lds_f(e32 + ((w.x >> 15) << 2));
+                A = fmaf(q, lds_f(r32 + ((w.x & 0x7FFFu) << 2)), A);
                 Bs += q;
-              }
+              });
             }
             if (s >= 0) {
               float raw = inv2 * (A + lu * Bs);
@@ -483,11 +505,10 @@ __global__ void __launch_bounds__(kNT, 1)
         load_row(t - 4, rn2);
         const float zinv = post ? ((kappa > 0.0 && kappa < 1e38) ? float(1.0 / kappa) : 0.f) : 0.f;
         {
-          const float *bt = vec + ct * S32;
+          const uint32_t b32 = smem_u32(vec + ct * S32), e32 = smem_u32(ebuf + cp * D_pad);
           float *bnew = vec + cp * S32;
-          const float *e = ebuf + cp * D_pad;
           const float *arow = trellis + size_t(f) * S32;  // alpha_f, backward-pack order
-          unsigned *bn = bins + (f & 1) * D_pad;
+          const uint32_t bn32 = smem_u32(bins + (f & 1) * D_pad);
           float dq = 0.f;
           int s_next = -1;
           float a_next = 0.f;
@@ -507,21 +528,18 @@ __global__ void __launch_bounds__(kNT, 1)
             const uint2 *sp = wp + __shfl_sync(kFull, my_base, i) + lane;
             float A = 0.f;
             if (post) {
-#pragma unroll 8
-              for (int j = 0; j < trips; ++j) {
-                const uint2 w = ldg_slot(sp + 32 * j);
-                const unsigned pdf = w.x >> 15;
-                const float term = __uint_as_float(w.y) * e[pdf] * (bt[w.x & 0x7FFFu] + ld);
+              tile_rows(sp, trips, [&](const uint2 w) {
+                const uint32_t pdf4 = (w.x >> 15) << 2;
+                const float term = __uint_as_float(w.y) * lds_f(e32 + pdf4) *
+                                   (lds_f(b32 + ((w.x & 0x7FFFu) << 2)) + ld);
                 A += term;
-                const unsigned fx = __float2uint_rn(as * term * kPostScale);
-                if (fx) atomicAdd(bn + pdf, fx);
-              }
+                red_add_shared_nz(bn32 + pdf4, __float2uint_rn(as * term * kPostScale));
+              });
             } else {
-#pragma unroll 8
-              for (int j = 0; j < trips; ++j) {
-                const uint2 w = ldg_slot(sp + 32 * j);
-                A += __uint_as_float(w.y) * e[w.x >> 15] * (bt[w.x & 0x7FFFu] + ld);
-              }
+              tile_rows(sp, trips, [&](const uint2 w) {
+                A += __uint_as_float(w.y) * lds_f(e32 + ((w.x >> 15) << 2)) *
+                     (lds_f(b32 + ((w.x & 0x7FFFu) << 2)) + ld);
+              });
             }
             if (s >= 0) {
               const float v = inv * A;
@@ -554,7 +572,8 @@ __global__ void __launch_bounds__(kNT, 1)
   }
 }
 
-int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st) {
+int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st,
+                        bool ring_only) {
   if (!g->streamable) return set_error(LFMMI_ERR_UNSUPPORTED, "graph has no stream pack");
   if (a.leak_pi) return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: uniform leak only");
   if (a.D > kMaxD) return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: D > 2048");
@@ -563,28 +582,34 @@ int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   const int S32 = (g->max_states + 31) & ~31;
   if (2 * S32 < 2 * a.B || g->max_stiles > 32 * kNW)
     return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: batch / graph shape");
-  const SSLayout lay = ss_layout(S32, a.D_pad, a.T_pad);
+  const Options &opt = options();
+  // TMA ring when its table holds a warp's chunks and it fits next to the columns
+  const int tiles_per_warp = (g->max_stiles + kNW - 1) / kNW;
+  const int max_deg = std::max(g->max_in_deg, g->max_out_deg);
+  bool ring = opt.stream_ring != 0 && ring_chunks_needed(tiles_per_warp, max_deg, 8) <= 64 &&
+              ss_layout(S32, a.D_pad, a.T_pad, true).total <= unsigned(kMaxSmem);
+  if (ring_only && !ring) return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: no ring");
+  const SSLayout lay = ss_layout(S32, a.D_pad, a.T_pad, ring);
   if (lay.total > unsigned(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,
                      "stream split needs " + std::to_string(lay.total) + " B shared memory");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const Options &opt = options();
   // every SM pair but two (the numerator pass runs beside this one)
   int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 2);
   nc = std::max(1, std::min(nc, std::min(96, sms / 2)));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > std::min(96, sms / 2))
     return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: too many utterances per cluster");
-  static bool configured = false;
-  if (!configured) {
-    const int rc = check_cuda(cudaFuncSetAttribute(fb_streamsplit_kernel,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kMaxSmem),
-                              "cudaFuncSetAttribute(stream split)");
+  auto kern = ring ? fb_streamsplit_kernel<true> : fb_streamsplit_kernel<false>;
+  static bool configured[2] = {false, false};
+  if (!configured[ring]) {
+    const int rc = check_cuda(
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
+        "cudaFuncSetAttribute(stream split)");
     if (rc) return rc;
-    configured = true;
+    configured[ring] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * nc);
@@ -598,9 +623,10 @@ int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  note_den_kernel("fb_streamsplit_kernel (2-CTA cluster: forward | backward, L2 packs)");
+  note_den_kernel(ring ? "fb_streamsplit_kernel (2-CTA cluster: forward | backward, TMA slot ring)"
+                       : "fb_streamsplit_kernel (2-CTA cluster: forward | backward, L2 packs)");
   const int hnum = std::max(1, std::min(63, opt.split_h64));
-  return check_cuda(cudaLaunchKernelEx(&cfg, fb_streamsplit_kernel, a, S32, lay, nc, hnum),
+  return check_cuda(cudaLaunchKernelEx(&cfg, kern, a, S32, lay, nc, hnum),
                     "fb_streamsplit_kernel launch");
 }
 

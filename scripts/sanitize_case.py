@@ -11,6 +11,8 @@ Cases pick the kernel under test with the library options (lfmmi_set_option):
   stream1  fb_stream_kernel<1024,1> reading slot rows straight from L2
   ring     fb_stream_kernel<1024,1> with its TMA slot ring (cp.async.bulk + mbarrier)
   ssplit   fb_streamsplit_kernel (forward | backward clusters, DSMEM scalars, kappa recursion)
+           with its TMA slot ring; ssplit0 the same reading slot rows from L2
+  hmm      phone-bigram den on fb_split_kernel with 8 lanes per state (xor-shuffle sums)
   numtile  numerators on the generic fb_tile_kernel<128> (linear kernel disabled)
 every case also runs the linear-chain numerator kernel (except numtile) and
 the combine kernel.  Utterances are short (<= 24 frames) to keep the
@@ -37,6 +39,8 @@ CASES = {
     "stream1": ("wsj_biphone", 2, dict(stream_mode="1024x1", stream_ring=0)),
     "ring": ("wsj_biphone", 2, dict(stream_mode="1024x1", stream_ring=1)),
     "ssplit": ("wsj_biphone", 3, dict(stream_mode="split")),
+    "ssplit0": ("wsj_biphone", 3, dict(stream_mode="split", stream_ring=0)),
+    "hmm": ("hmm", 3, dict()),
     "numtile": ("wsj_mono", 3, dict(linear=0)),
 }
 

@@ -122,7 +122,9 @@ def _kernel_env(kernel, lib_options):
     (tile kernel with one posterior slot buffer), "numtile" (numerators through
     the generic tile kernel instead of the linear-chain kernel), "smallnum" /
     "smallden" (the small-graph threshold moved either way), "g2" / "g4s" (tile
-    packs with 2 / 4 lanes per state on the tile / split kernels)."""
+    packs with 2 / 4 lanes per state on the tile / split kernels), "ssplit" /
+    "ssplit0" (L2-resident graphs on the stream split kernel, with / without
+    the TMA slot ring)."""
     if kernel == "tile":  # one CTA per utterance (no forward/backward split)
         lib_options(split=0)
     if kernel in ("split1", "split2"):  # 2-CTA split, several utterances per cluster
@@ -142,10 +144,15 @@ def _kernel_env(kernel, lib_options):
         lib_options(tile_g=2, split=0)
     if kernel == "g4s":  # four lanes per state, split kernel
         lib_options(tile_g=4, split=1)
+    if kernel == "ssplit":  # L2-resident graphs: forward | backward stream split (TMA ring)
+        lib_options(stream_mode="split")
+    if kernel == "ssplit0":  # ... slot rows straight from L2
+        lib_options(stream_mode="split", stream_ring=0)
 
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "noring",
-                                    "group", "smallnum", "smallden", "g2", "g4s"])
+                                    "group", "smallnum", "smallden", "g2", "g4s", "ssplit",
+                                    "ssplit0"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None), ("hmm", 24),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])
