@@ -100,19 +100,33 @@ struct SlotRing {
       mbar_wait(bar(g_cons), (g_cons / NSLOT) & 1u);
       const uint32_t sl = slot(g_cons) + unsigned(lane) * 8u;
       const int n = min(ROWS, trips - j0);
-      uint2 w[ROWS];
+      // two halves: the first half's arc bodies run while the second half's
+      // words are loaded, with half the word registers live (the 1024-thread
+      // kernels are capped at 64 registers and otherwise re-derive addresses)
+      constexpr int H = ROWS / 2 > 0 ? ROWS / 2 : 1;
+      uint2 w[H];
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r) w[r] = lds_v2(sl + unsigned(r) * 256u);
+      for (int r = 0; r < H; ++r) w[r] = lds_v2(sl + unsigned(r) * 256u);
+      if (n == ROWS) {
+#pragma unroll
+        for (int r = 0; r < H; ++r) body(w[r]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < H; ++r)
+          if (r < n) body(w[r]);
+      }
+#pragma unroll
+      for (int r = H; r < ROWS; ++r) w[r - H] = lds_v2(sl + unsigned(r) * 256u);
       __syncwarp();  // every lane has its words: the slot may be refilled
       ++g_cons;
       if (g_iss < g_end) issue();
       if (n == ROWS) {
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r) body(w[r]);
+        for (int r = H; r < ROWS; ++r) body(w[r - H]);
       } else {
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r)
-          if (r < n) body(w[r]);
+        for (int r = H; r < ROWS; ++r)
+          if (r < n) body(w[r - H]);
       }
     }
   }

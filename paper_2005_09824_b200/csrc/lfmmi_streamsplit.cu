@@ -48,7 +48,7 @@ namespace lfmmi {
 namespace {
 
 constexpr int kNT = 1024, kNW = kNT / 32;
-constexpr int kMaxD = 2048, kEPT = kMaxD / kNT;  // log-likelihood elements per thread
+constexpr int kMaxD = 2048, kEPT = (kMaxD + kNT - 1) / kNT;  // log-likelihood elements per thread
 constexpr float kPostScale = 268435456.f;        // 2^28
 constexpr int kMaxItems = 64;                    // utterances per cluster
 // TMA slot ring (as fb_stream_kernel): 2 chunks of 8 slot rows per warp
