@@ -586,10 +586,15 @@ def run_ours(args):
     peak = peak or 6650.0
     achieved = A / (kernel_ms / 1e3) / 1e9
     ncu = load_json(NCU_SUMMARY) or {}
-    # ncu traffic is recorded for the headline workload only (profiles/ncu_summary.json)
+    # ncu traffic per launch of the dominant kernel (profiles/ncu_summary.json):
+    # the headline workload's den kernel, the biphone stream split ("ss") and
+    # the hmm den ("hmm") captures of scripts/gpu_final.sh
     traffic = None
-    if ncu.get("workload", "wsj_mono") == args.config and args.batch is None:
-        traffic = ncu.get("den_dram_bytes_per_launch")
+    if args.batch is None:
+        key = {ncu.get("workload", "wsj_mono"): "den", "wsj_biphone": "ss", "hmm": "hmm"}.get(
+            args.config)
+        if key:
+            traffic = ncu.get(f"{key}_dram_bytes_per_launch")
 
     # ---- end-to-end through the public API with host buffers ----------------
     e2e = None

@@ -31,6 +31,21 @@ def main(tag):
         if os.path.exists(p):
             lines += [l for l in open(p) if l.startswith("{")]
     open(os.path.join(P, f"{tag}_bench.jsonl"), "w").writelines(lines)
+    # every config of gpu_final.sh (ours + reference arm), one line each
+    cfg = []
+    for c in ("wsj_mono", "toy", "hmm", "wsj_biphone", "large", "sweep", "sweep128"):
+        for f in ((f"bench_{c}.log", f"bench_ref_{c}.log") if c != "wsj_mono" else
+                  ("bench.log", "bench_ref.log")):
+            p = os.path.join(G, f)
+            if os.path.exists(p):
+                cfg += [l for l in open(p) if l.startswith("{")]
+    if cfg:
+        open(os.path.join(P, f"{tag}_configs.jsonl"), "w").writelines(cfg)
+    for f, keep in (("pytest_gpu.log", 12), ("smoke.log", 20), ("sanitizers.log", 20)):
+        p = os.path.join(G, f)
+        if os.path.exists(p):
+            tail = open(p).read().splitlines()[-keep:]
+            open(os.path.join(P, f"{tag}_{f}"), "w").write("\n".join(tail) + "\n")
     if os.path.exists(os.path.join(G, "host.txt")):
         open(os.path.join(P, f"{tag}_host.txt"), "w").write(open(os.path.join(G, "host.txt")).read())
     lc = os.path.join(G, "launches.csv")
@@ -47,7 +62,7 @@ def main(tag):
     summ = {"round": tag, "workload": "wsj_mono",
             "source": "ncu --set full --clock-control none; bench.py --profile (wsj_mono, seed 0)"}
     txt = []
-    for name in ("den", "num", "chain"):
+    for name in ("den", "num", "chain", "ss", "hmm"):
         rep = os.path.join(G, f"prof_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -60,6 +75,8 @@ def main(tag):
                                   capture_output=True, text=True).stdout)
         txt.append(subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_lines.py"), rep, "30"],
                                   capture_output=True, text=True).stdout)
+        txt.append(subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_lines_src.py"), rep,
+                                   "30"], capture_output=True, text=True).stdout)
     open(os.path.join(P, f"{tag}_ncu_full_summary.txt"), "w").write("\n".join(txt))
     json.dump(summ, open(os.path.join(P, "ncu_summary.json"), "w"), indent=1)
     print(json.dumps(summ, indent=1))
