@@ -145,7 +145,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   h.desc.resize(size_t(num_rows) * kDescInts, 0);
   const GatherLayout gl = make_gather_layout(max_states, num_pdfs);
   int max_chunks = 0, max_in = 0, max_out = 0;
-  int max_tiles = 0, max_tf = 0, max_tb = 0, max_xpad = 0;
+  int max_tiles = 0, max_tf = 0, max_tb = 0, max_xpad = 0, max_tile_g = 1;
   bool all_tileable = true;
   bool all_streamable = true;
   bool all_linear = true;
@@ -407,6 +407,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
       TileSchedule tb = schedule_tiles(S, optr, &h.out_dst[a0], &h.out_pdf[a0], &h.out_p64[a0],
                                        gl, true, -1, G);
       d[kTileG] = G;
+      max_tile_g = std::max(max_tile_g, G);
       d[kNTiles] = int(tf.trips.size());
       std::vector<int> pptr, xslot;
       int xpad = 0;
@@ -530,6 +531,7 @@ extern "C" int lfmmi_graphs_create(int32_t num_rows, int32_t max_states, int32_t
   g->max_in_deg = max_in;
   g->max_out_deg = max_out;
   g->max_tiles = max_tiles;
+  g->max_tile_g = max_tile_g;
   g->max_tf_slots = max_tf;
   g->max_tb_slots = max_tb;
   g->tileable = all_tileable;

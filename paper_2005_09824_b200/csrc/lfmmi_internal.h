@@ -98,6 +98,7 @@ struct lfmmi_graphs {
   bool linear = false;      // every row is a linear chain (fb_linear_kernel pack present)
   bool linear_only = false; // lfmmi_graphs_create_linear: nothing but the linear pack
   int32_t max_stiles = 0;
+  int32_t max_tile_g = 1;   // largest kTileG of the rows (1: one lane per state everywhere)
   int32_t rep_r = 1, r_stride = 0, rep_e = 1, e_stride = 0;  // gather-vector replication
   void *device_block = nullptr;
   size_t device_bytes = 0;

@@ -101,7 +101,9 @@ __device__ __forceinline__ void cluster_barrier() {
 // graphs (<= 16 tiles, e.g. a 43-state phone-bigram den with 8 lanes per state):
 // 128-thread CTAs, several clusters per SM pair, one utterance per cluster,
 // tiles dealt to the warps in snake order.
-template <int kNW>
+// kGrp: some row's tile packs have G > 1 lanes per state (partial sums over G
+// lanes); compiled out otherwise.
+template <int kNW, bool kGrp>
 __global__ void __launch_bounds__(32 * kNW, 16 / kNW)
     fb_split_kernel(const FBArgs<float> a, int Fmax, int ntiles_max, int X_pad, int nclusters,
                     int hnum) {
@@ -472,8 +474,8 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW)
                 fwd_tile_f32<false>(wp32 + uint32_t(base) * 8u, trips, e32, r32, A, Bs);
               raw = inv2 * (A + lu * Bs);
             }
-            raw = group_sum(raw, G);
-            if (s != 0xFFFF && lead) {
+            if constexpr (kGrp) raw = group_sum(raw, G);
+            if (s != 0xFFFF && (!kGrp || lead)) {
               if (last) raw *= fin[s];
               put_vec(rn, s, raw);
               psum += raw;
@@ -641,8 +643,8 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW)
               } else {
                 A = bwd_plain_tile_f32(wp32 + uint32_t(base) * 8u, trips, e32, b32, ld);
               }
-              A = group_sum(A, G);
-              if (s != 0xFFFF && lead) {
+              if constexpr (kGrp) A = group_sum(A, G);
+              if (s != 0xFFFF && (!kGrp || lead)) {
                 const float v = inv * A;
                 put_vec(bn, s, v);
                 dq = fmaf(upi, v, dq);
@@ -735,14 +737,16 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   nc = std::max(1, std::min(nc, cap));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > cap) return set_error(LFMMI_ERR_UNSUPPORTED, "split: too many utterances per cluster");
-  auto kern = small ? fb_split_kernel<4> : fb_split_kernel<16>;
-  static bool configured[2] = {false, false};
-  if (!configured[small]) {
+  const bool grp = g->max_tile_g > 1;
+  auto kern = small ? (grp ? fb_split_kernel<4, true> : fb_split_kernel<4, false>)
+                    : (grp ? fb_split_kernel<16, true> : fb_split_kernel<16, false>);
+  static bool configured[4] = {false, false, false, false};
+  if (!configured[2 * small + grp]) {
     int rc = check_cuda(
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
         "cudaFuncSetAttribute(split)");
     if (rc) return rc;
-    configured[small] = true;
+    configured[2 * small + grp] = true;
   }
   const int hnum = std::max(0, std::min(64, opt.split_h64));  // midpoint in 64ths of T
   cudaLaunchConfig_t cfg{};

@@ -417,52 +417,63 @@ __global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks 
       (void)e32;
       (void)r32;
       Real psum = Real(0);
-      for (int rr = wlo; rr < whi; ++rr) {
-        const int tile = tile_at(rr);
-        if (!XDB && tile >= ntiles) continue;
-        const unsigned info = tinfo[tile * 32 + lane];
-        const int trips = ttrips[tile];
-        const int base = tbase[tile] + lane;
-        Real A = Real(0), Bs = Real(0);
-        if constexpr (FAST) {
-          const uint32_t sb = wp32 + uint32_t(base) * 8u;
-          if (leakc != Real(0))
-            fwd_tile_f32<true>(sb, trips, e32, r32, A, Bs);
-          else
-            fwd_tile_f32<false>(sb, trips, e32, r32, A, Bs);
-        } else if (leakc != Real(0)) {
-#pragma unroll 4
-          for (int j = 0; j < trips; ++j) {
-            unsigned wd;
-            Real p;
-            slot.load(base + 32 * j, wd, p);
-            const Real w = p * e[wd >> 16];
-            const int src = int(wd & 0xFFFFu);
-            A = fma(w, r[src], A);
-            if constexpr (CUSTOM_PI)  // gather index may name copy 1 (rep_r <= 2)
-              Bs = fma(w, pi[src >= a.r_stride ? src - a.r_stride : src], Bs);
+      // G lanes per state (kTileG) only for small graphs: the partial-sum
+      // shuffles and the group-leader test compiled out of the G = 1 loop
+      auto tiles = [&](auto grp) {
+        constexpr bool GRP = decltype(grp)::value;
+        for (int rr = wlo; rr < whi; ++rr) {
+          const int tile = tile_at(rr);
+          if (!XDB && tile >= ntiles) continue;
+          const unsigned info = tinfo[tile * 32 + lane];
+          const int trips = ttrips[tile];
+          const int base = tbase[tile] + lane;
+          Real A = Real(0), Bs = Real(0);
+          if constexpr (FAST) {
+            const uint32_t sb = wp32 + uint32_t(base) * 8u;
+            if (leakc != Real(0))
+              fwd_tile_f32<true>(sb, trips, e32, r32, A, Bs);
             else
-              Bs += w;
+              fwd_tile_f32<false>(sb, trips, e32, r32, A, Bs);
+          } else if (leakc != Real(0)) {
+  #pragma unroll 4
+            for (int j = 0; j < trips; ++j) {
+              unsigned wd;
+              Real p;
+              slot.load(base + 32 * j, wd, p);
+              const Real w = p * e[wd >> 16];
+              const int src = int(wd & 0xFFFFu);
+              A = fma(w, r[src], A);
+              if constexpr (CUSTOM_PI)  // gather index may name copy 1 (rep_r <= 2)
+                Bs = fma(w, pi[src >= a.r_stride ? src - a.r_stride : src], Bs);
+              else
+                Bs += w;
+            }
+          } else {
+  #pragma unroll 4
+            for (int j = 0; j < trips; ++j) {
+              unsigned wd;
+              Real p;
+              slot.load(base + 32 * j, wd, p);
+              A = fma(p * e[wd >> 16], r[wd & 0xFFFFu], A);
+            }
           }
-        } else {
-#pragma unroll 4
-          for (int j = 0; j < trips; ++j) {
-            unsigned wd;
-            Real p;
-            slot.load(base + 32 * j, wd, p);
-            A = fma(p * e[wd >> 16], r[wd & 0xFFFFu], A);
+          const int s = int(info & 0xFFFFu);
+          if constexpr (GRP) {
+            A = group_sum(A, G);
+            Bs = group_sum(Bs, G);
+          }
+          if (s != 0xFFFF && (!GRP || lead)) {
+            Real raw = inv2 * (A + leakc * (CUSTOM_PI ? Bs : upi * Bs));
+            if (last) raw *= fin[s];
+            put_vec(rn, s, raw);
+            psum += raw;
           }
         }
-        const int s = int(info & 0xFFFFu);
-        A = group_sum(A, G);
-        Bs = group_sum(Bs, G);
-        if (s != 0xFFFF && lead) {
-          Real raw = inv2 * (A + leakc * (CUSTOM_PI ? Bs : upi * Bs));
-          if (last) raw *= fin[s];
-          put_vec(rn, s, raw);
-          psum += raw;
-        }
-      }
+      };
+      if (G > 1)
+        tiles(std::true_type{});
+      else
+        tiles(std::false_type{});
       psum = warp_sum(psum);
       if (lane == 0) part[nxt * 32 + warp] = psum;
     }
@@ -610,36 +621,45 @@ __global__ void __launch_bounds__(GROUP *IPC, GROUP *IPC <= 128 ? kNumMinBlocks 
       Real *bn = rbuf + cp * RB;
       Real *xt = xterm + xb * X_pad;
       Real dp = Real(0);
-      for (int rr = wlo; rr < whi; ++rr) {
-        const int tile = tile_at(rr);
-        if (!XDB && tile >= ntiles) continue;
-        const unsigned info = tinfo[tile * 32 + lane];
-        const int trips = ttrips[tile];
-        const int base = tbase[tile] + lane;
-        const int s = int(info & 0xFFFFu);
-        const Real as = (s != 0xFFFF) ? al[s] * inv : Real(0);
-        Real A = Real(0);
-        if constexpr (FAST) {
-          A = bwd_tile_f32(wp32 + uint32_t(base) * 8u, xs32 + uint32_t(base) * 2u, trips,
-                           smem_u32(e), smem_u32(bt), smem_u32(xt), ld, as);
-        } else {
-#pragma unroll 4
-          for (int j = 0; j < trips; ++j) {
-            unsigned wd;
-            Real p;
-            slot.load(base + 32 * j, wd, p);
-            const Real term = p * e[wd >> 16] * (bt[wd & 0xFFFFu] + ld);
-            A += term;
-            xt[XS[base + 32 * j]] = as * term;
+      // G lanes per state (kTileG) only for small graphs: the partial-sum
+      // shuffles and the group-leader test compiled out of the G = 1 loop
+      auto tiles = [&](auto grp) {
+        constexpr bool GRP = decltype(grp)::value;
+        for (int rr = wlo; rr < whi; ++rr) {
+          const int tile = tile_at(rr);
+          if (!XDB && tile >= ntiles) continue;
+          const unsigned info = tinfo[tile * 32 + lane];
+          const int trips = ttrips[tile];
+          const int base = tbase[tile] + lane;
+          const int s = int(info & 0xFFFFu);
+          const Real as = (s != 0xFFFF) ? al[s] * inv : Real(0);
+          Real A = Real(0);
+          if constexpr (FAST) {
+            A = bwd_tile_f32(wp32 + uint32_t(base) * 8u, xs32 + uint32_t(base) * 2u, trips,
+                             smem_u32(e), smem_u32(bt), smem_u32(xt), ld, as);
+          } else {
+  #pragma unroll 4
+            for (int j = 0; j < trips; ++j) {
+              unsigned wd;
+              Real p;
+              slot.load(base + 32 * j, wd, p);
+              const Real term = p * e[wd >> 16] * (bt[wd & 0xFFFFu] + ld);
+              A += term;
+              xt[XS[base + 32 * j]] = as * term;
+            }
+          }
+          if constexpr (GRP) A = group_sum(A, G);
+          if (s != 0xFFFF && (!GRP || lead)) {
+            const Real v = inv * A;
+            put_vec(bn, s, v);
+            dp = fma(CUSTOM_PI ? pi[s] : upi, v, dp);
           }
         }
-        A = group_sum(A, G);
-        if (s != 0xFFFF && lead) {
-          const Real v = inv * A;
-          put_vec(bn, s, v);
-          dp = fma(CUSTOM_PI ? pi[s] : upi, v, dp);
-        }
-      }
+      };
+      if (G > 1)
+        tiles(std::true_type{});
+      else
+        tiles(std::false_type{});
       dp = warp_sum(dp);
       if (lane == 0) part[cp * 32 + warp] = dp;
     }
