@@ -53,8 +53,7 @@ const char *lfmmi_last_error(void);
  * Names: tile, stream, linear (0/1: kernel families the dispatcher may use),
  * linear_split (numerators as forward | backward warps), emit (emissions
  * pre-pass), split (-1 auto / 0 off / 1 force), split_clusters (0 auto),
- * split_h64, split_small (4-warp split CTAs for graphs of <= 16 tiles),
- * tile_g (tile-pack lanes per state, 0 auto; pack time), stream_mode ("auto", "split", "1024x1", "1024x2", "512x2"),
+ * split_h64, tile_g (tile-pack lanes per state, 0 auto; pack time), stream_mode ("auto", "split", "1024x1", "1024x2", "512x2"),
  * stream_ring (TMA slot ring), num_group, small_arcs (graphs with <= 512
  * states and <= small_arcs arcs take the numerator-sized kernels), tile_xdb,
  * serial (-1 auto / 0 / 1:

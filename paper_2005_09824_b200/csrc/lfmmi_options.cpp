@@ -26,7 +26,6 @@ const Field kFields[] = {
     {"split", &Options::split, nullptr},
     {"split_clusters", &Options::split_clusters, nullptr},
     {"split_h64", &Options::split_h64, nullptr},
-    {"split_small", &Options::split_small, nullptr},
     {"stream_mode", nullptr, &Options::stream_mode},
     {"stream_ring", &Options::stream_ring, nullptr},
     {"num_group", &Options::num_group, nullptr},

@@ -18,7 +18,6 @@ struct Options {
   int split = -1;         // denominator split kernel: -1 auto (B <= 2 x SMs), 0 off, 1 force
   int split_clusters = 0; // 0 = auto
   int split_h64 = 33;     // split midpoint in 64ths of T
-  int split_small = 1;    // split kernel: 4-warp CTAs for graphs with <= 16 tiles (0 off)
   std::string stream_mode = "auto";  // "auto" | "1024x1" | "1024x2" | "512x2"
   int stream_ring = 1;    // stream kernel: TMA slot ring when it fits (biphone 9.45 vs 9.96 ms)
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel

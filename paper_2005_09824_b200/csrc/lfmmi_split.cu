@@ -48,7 +48,8 @@ namespace lfmmi {
 
 namespace {
 
-constexpr int kMaxClusters = 128;             // LPT bins of the in-kernel assignment
+constexpr int kNW = 16, kNT = 32 * kNW;
+constexpr int kMaxClusters = 96;              // LPT bins of the in-kernel assignment
 constexpr int kLptWords = (kMaxClusters + 31) / 32;
 constexpr int kRowAhead = 4, kStageRing = 8;  // log-likelihood row pipeline (as fb_tile_kernel)
 constexpr int kRing = 3, kRingAhead = 2;      // other CTA's trellis rows: issued 2 frames ahead
@@ -97,18 +98,14 @@ __device__ __forceinline__ void cluster_barrier() {
 
 }  // namespace
 
-// kNW = 16: WSJ-sized graphs, host LPT warp lists (chores biased).  kNW = 4: small
-// graphs (<= 16 tiles, e.g. a 43-state phone-bigram den with 8 lanes per state):
-// 128-thread CTAs, several clusters per SM pair, one utterance per cluster,
-// tiles dealt to the warps in snake order.
 // kGrp: some row's tile packs have G > 1 lanes per state (partial sums over G
-// lanes); compiled out otherwise.
-template <int kNW, bool kGrp>
-__global__ void __launch_bounds__(32 * kNW, 16 / kNW)
+// lanes); compiled out otherwise.  (A 4-warp variant for small graphs — one
+// cluster per utterance, several per SM — measured slower on the 43-state hmm
+// den: 0.77 vs 0.61 ms.)
+template <bool kGrp>
+__global__ void __launch_bounds__(kNT, 1)
     fb_split_kernel(const FBArgs<float> a, int Fmax, int ntiles_max, int X_pad, int nclusters,
                     int hnum) {
-  constexpr int kNT = 32 * kNW;
-  constexpr bool kLists = kNW == kTableNW;  // host LPT warp lists exist for 16 warps
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ctid = kNT - 1 - tid, cwarp = ctid >> 5;  // chores on the last warps
@@ -292,17 +289,7 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW)
     }
     // forward CTA: LPT lists without / with the flush chore (first / second half)
     const int *wl = wl1;
-    const int nt_item = desc[kNTiles];
-    int wlo = 0, whi = (nt_item + kNW - 1) / kNW;
-    if constexpr (kLists) {
-      wlo = wt1[warp];
-      whi = wt1[warp + 1];
-    }
-    // r-th tile of this warp: host list, or snake order (heavy tiles first)
-    auto tile_at = [&](int r) {
-      if constexpr (kLists) return wl[r];
-      return r * kNW + ((r & 1) ? kNW - 1 - warp : warp);
-    };
+    int wlo = wt1[warp], whi = wt1[warp + 1];
 
     const int nrw = (D + 31) / 32 < kNW ? (D + 31) / 32 : kNW;  // chore warps (row elements)
     auto issue_row = [&](int t) {
@@ -452,8 +439,7 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW)
           const bool last = (k + 1 == T);
           float psum = 0.f;
           for (int rr = wlo; rr < whi; ++rr) {
-            const int tile = tile_at(rr);
-            if (!kLists && tile >= nt_item) continue;
+            const int tile = wl[rr];
             const unsigned info = tinfo[tile * 32 + lane];
             const int trips = ttrips[tile];
             const int base = tbase[tile] + lane;
@@ -506,11 +492,9 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW)
           cp_async_commit();
           cp_async_wait<0>();
           __syncthreads();
-          if constexpr (kLists) {
-            wl = wl2;
-            wlo = wt2[warp];
-            whi = wt2[warp + 1];
-          }
+          wl = wl2;
+          wlo = wt2[warp];
+          whi = wt2[warp + 1];
         }
         stamp(3);
         if (!other_failed)
@@ -628,8 +612,7 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW)
             float *bn = rbuf + cpar * RB;
             float dq = 0.f;
             for (int rr = wlo; rr < whi; ++rr) {
-              const int tile = tile_at(rr);
-              if (!kLists && tile >= nt_item) continue;
+              const int tile = wl[rr];
               const unsigned info = tinfo[tile * 32 + lane];
               const int trips = ttrips[tile];
               const int base = tbase[tile] + lane;
@@ -723,35 +706,26 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   // / 1.083 / 1.082 / 1.082 ms with 66 / 68 / 69 / 70 / 71 / 72 clusters, 1.19 ms
   // with 74 — numerators then wait for free SMs); beyond that LPT pairs long
   // with short utterances.  Option split_clusters overrides.
-  //
-  // Small graphs (<= 16 tiles: 4 warps deal them in <= 4 rounds) whose layout
-  // leaves room for >= 2 CTAs per SM take 128-thread CTAs instead: the
-  // per-frame barrier, reductions and chores of 16 warps dominate a 43-state
-  // den (~2k cycles per frame), and every utterance gets its own cluster.
-  const bool small = opt.split_small != 0 && g->max_tiles <= 16 &&
-                     2 * lay.total <= size_t(kMaxSmem);
   const int reserve = a.reserve_sms > 0 ? a.reserve_sms : 6;
-  const int cap = small ? kMaxClusters : std::min(96, sms / 2);
-  int nc = opt.split_clusters > 0 ? opt.split_clusters
-                                  : (small ? a.B : std::min(a.B, (sms - reserve) / 2));
+  const int cap = std::min(kMaxClusters, sms / 2);
+  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, (sms - reserve) / 2);
   nc = std::max(1, std::min(nc, cap));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > cap) return set_error(LFMMI_ERR_UNSUPPORTED, "split: too many utterances per cluster");
   const bool grp = g->max_tile_g > 1;
-  auto kern = small ? (grp ? fb_split_kernel<4, true> : fb_split_kernel<4, false>)
-                    : (grp ? fb_split_kernel<16, true> : fb_split_kernel<16, false>);
-  static bool configured[4] = {false, false, false, false};
-  if (!configured[2 * small + grp]) {
+  auto kern = grp ? fb_split_kernel<true> : fb_split_kernel<false>;
+  static bool configured[2] = {false, false};
+  if (!configured[grp]) {
     int rc = check_cuda(
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem),
         "cudaFuncSetAttribute(split)");
     if (rc) return rc;
-    configured[2 * small + grp] = true;
+    configured[grp] = true;
   }
   const int hnum = std::max(0, std::min(64, opt.split_h64));  // midpoint in 64ths of T
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * nc);
-  cfg.blockDim = dim3(small ? 128 : 512);
+  cfg.blockDim = dim3(kNT);
   cfg.dynamicSmemBytes = lay.total;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -767,8 +741,7 @@ int launch_split<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
     std::fprintf(stderr, "[lfmmi] split: %d clusters (max active %d), smem %zu (scales %s)\n", nc,
                  maxc, lay.total, b.sc_smem ? "smem" : "hbm");
   }
-  note_den_kernel(small ? "fb_split_kernel<4 warps> (2-CTA cluster: forward | backward)"
-                        : "fb_split_kernel (2-CTA cluster: forward | backward)");
+  note_den_kernel("fb_split_kernel (2-CTA cluster: forward | backward)");
   if (opt.profile != "split")
     return check_cuda(cudaLaunchKernelEx(&cfg, kern, b, Fmax, g->max_tiles, X_pad, nc, hnum),
                       "fb_split_kernel launch");
