@@ -66,6 +66,17 @@ __device__ __forceinline__ float exp_r(float x) { return expf(x); }
 // Correctly rounded reciprocal (== 1 / x in IEEE round-to-nearest), no division subroutine.
 __device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+// One MUFU.RCP (rel. error ~2^-23, subnormals kept) for per-frame normalisers
+// of the split kernel: a column scaled by (1 + e) / t instead of 1 / t is
+// renormalised by the next frame's sum, so the forward log-probability (sum of
+// log t) picks up sum log(1 + e) <= T 2^-23 (~4e-5 absolute at T = 300, far
+// inside the fp32 objective bar), and posteriors, divided by their frame total
+// Z, do not see the backward normaliser at all.
+__device__ __forceinline__ float rcp_fast(float x) {
+  float y;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ double exp_r(double x) { return exp(x); }
 
 // ---- cp.async (LDGSTS) -----------------------------------------------------

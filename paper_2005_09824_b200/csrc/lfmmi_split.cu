@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kNT, 1)
             fail_at = k - 1;
             return false;
           }
-          inv2 = rcp_rn(t2);
+          inv2 = rcp_fast(t2);
           if (tid == 0) scales[k - 1] = t2;
         }
         const float lu = leakc * upi;
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kNT, 1)
           const float t0 = lane_sum<kNW>(part + ct * 32, lane);  // mean of the raw column
           const float ld = (t < T && lam > 0.f) ? lam * t0 : 0.f;
           const float n = float(S) * t0;
-          const float inv = (n > 0.f && !isinf(n)) ? rcp_rn(n) : 1.f;
+          const float inv = (n > 0.f && !isinf(n)) ? rcp_fast(n) : 1.f;
           if constexpr (!POST) {  // beta'_f for the forward CTA's posteriors
             const float4 *r4 = reinterpret_cast<const float4 *>(rbuf + ct * RB);
             float4 *b4 = reinterpret_cast<float4 *>(trellis + size_t(f) * S_pad);
