@@ -81,6 +81,7 @@ struct SlotRing {
         if (lane == 0 && c < CHUNKS)
           ctab[c] = make_uint2(unsigned(bs + 32 * j0), unsigned(min(ROWS, tr - j0)) * 256u);
     }
+    if (c > CHUNKS) __trap();  // launcher bug: the table cannot hold this warp's chunks
     nchunk = c;
     __syncwarp();
     g_end = g_iss + unsigned(c) * unsigned(max(frames, 0));
