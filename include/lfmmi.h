@@ -54,7 +54,8 @@ const char *lfmmi_last_error(void);
  * linear_split (numerators as forward | backward warps), emit (emissions
  * pre-pass), split (-1 auto / 0 off / 1 force), split_clusters (0 auto),
  * split_h64, tile_g (tile-pack lanes per state, 0 auto; pack time), stream_mode ("auto", "split", "1024x1", "1024x2", "512x2"),
- * stream_ring (TMA slot ring), num_group, small_arcs (graphs with <= 512
+ * stream_ring (TMA slot ring), num_group, tile_persist (den tile kernel with
+ * more utterances than SMs: persistent CTAs over an in-kernel LPT), small_arcs (graphs with <= 512
  * states and <= small_arcs arcs take the numerator-sized kernels), tile_xdb,
  * serial (-1 auto / 0 / 1:
  * numerator pass before the denominator pass), sched_iters (-1 auto),

@@ -203,6 +203,7 @@ struct FBArgs {
   const Real *E;
   const Real *Em;
   int reserve_sms;  // split den kernel: SMs to leave to the concurrent numerator pass (0: default)
+  int persist;      // tile den kernel: > 0 = that many persistent CTAs, utterances by in-kernel LPT
 };
 
 }  // namespace lfmmi

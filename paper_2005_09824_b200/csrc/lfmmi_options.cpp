@@ -31,6 +31,7 @@ const Field kFields[] = {
     {"num_group", &Options::num_group, nullptr},
     {"small_arcs", &Options::small_arcs, nullptr},
     {"tile_xdb", &Options::tile_xdb, nullptr},
+    {"tile_persist", &Options::tile_persist, nullptr},
     {"serial", &Options::serial, nullptr},
     {"emit", &Options::emit, nullptr},
     {"sched_iters", &Options::sched_iters, nullptr},

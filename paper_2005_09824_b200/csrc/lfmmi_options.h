@@ -23,6 +23,8 @@ struct Options {
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
   int small_arcs = 1024;  // graphs with <= 512 states AND <= this many arcs per row take the
                           // numerator-sized kernels; denser ones (a phone-bigram den) the den path
+  int tile_persist = 0;  // den tile kernel, B > SMs: persistent CTAs over an in-kernel LPT
+                         // (0 off, >= 2: force that many CTAs — tests)
   int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots
   int serial = 0;         // chain_loss: numerator pass before the den pass (-1 auto: B > 2 x SMs)
   int emit = 1;           // chain_loss (fp32): emissions pre-pass shared by the passes

@@ -31,6 +31,7 @@
 
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
+#include "lfmmi_lpt.cuh"
 #include "lfmmi_options.h"
 #include "lfmmi_schedule.h"
 #include "lfmmi_tile_common.cuh"
@@ -49,12 +50,11 @@ namespace lfmmi {
 namespace {
 
 constexpr int kNW = 16, kNT = 32 * kNW;
-constexpr int kMaxClusters = 96;              // LPT bins of the in-kernel assignment
-constexpr int kLptWords = (kMaxClusters + 31) / 32;
+constexpr int kMaxClusters = 96;              // clusters (LPT bins) per launch
 constexpr int kRowAhead = 4, kStageRing = 8;  // log-likelihood row pipeline (as fb_tile_kernel)
 constexpr int kRing = 3, kRingAhead = 2;      // other CTA's trellis rows: issued 2 frames ahead
 constexpr int kWait = 1;                      // groups still in flight at the end of a frame
-constexpr int kMaxItems = 64;                 // utterances per cluster (launcher guarantees)
+constexpr int kMaxItems = kLptMaxItems;       // utterances per cluster (launcher guarantees)
 
 struct SplitLayout {
   size_t wp, xs, tinfo, ttrips, tbase, wlist, wtab, wlist2, wtab2, pdfptr, xterm, rbuf, ring, ebuf, stage,
@@ -137,52 +137,10 @@ __global__ void __launch_bounds__(kNT, 1)
   const float lam = a.leak;
   const bool fwd = role == 0;
 
-  // ---- this cluster's utterances: LPT over the clusters, longest first --------------
-  // (every CTA computes the same assignment; lengths / order staged in xterm)
-  {
-    int *lens = reinterpret_cast<int *>(xterm);
-    int *order = lens + a.B;
-    for (int i = tid; i < a.B; i += kNT) lens[i] = item_frames(a.lengths, i, a.T_max);
-    __syncthreads();
-    for (int i = tid; i < a.B; i += kNT) {
-      const int ti = lens[i];
-      int r = 0;
-      for (int j = 0; j < a.B; ++j) {
-        const int tj = lens[j];
-        r += (tj > ti) | ((tj == ti) & (j < i));
-      }
-      order[r] = i;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      unsigned load[kLptWords] = {};
-      int cnt[kLptWords] = {};
-      int mine = 0;
-      for (int r = 0; r < a.B; ++r) {
-        const int i = order[r];
-        unsigned key = 0xFFFFFFFFu;
-#pragma unroll
-        for (int q = 0; q < kLptWords; ++q) {
-          const int bin = lane + 32 * q;
-          if (bin < nclusters && cnt[q] < kMaxItems) key = min(key, (load[q] << 7) | unsigned(bin));
-        }
-        const unsigned best = __reduce_min_sync(kFull, key);
-        const int bin = int(best & 127u);
-#pragma unroll
-        for (int q = 0; q < kLptWords; ++q)
-          if (lane + 32 * q == bin) {
-            load[q] += unsigned(lens[i] + 4);  // + prologue / barrier overhead (frames)
-            ++cnt[q];
-          }
-        if (bin == cluster) {
-          if (lane == 0) items[4 + mine] = i;
-          ++mine;
-        }
-      }
-      if (lane == 0) items[0] = mine;
-    }
-    __syncthreads();
-  }
+  // ---- this cluster's utterances: LPT over the clusters, longest first (every CTA
+  // computes the same assignment; lengths / order staged in the slot buffers)
+  lpt_assign<kNT>(a.lengths, a.B, a.T_max, nclusters, cluster, 4,
+                  reinterpret_cast<int *>(xterm), items);
   const int nitems = items[0];
 
   // ---- the arc pack of this CTA's direction (reloaded only when the row changes) -----

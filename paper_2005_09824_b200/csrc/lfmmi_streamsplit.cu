@@ -38,6 +38,7 @@
 
 #include "lfmmi_device.cuh"
 #include "lfmmi_kernels.h"
+#include "lfmmi_lpt.cuh"
 #include "lfmmi_options.h"
 #include "lfmmi_ring.cuh"
 #include "lfmmi_tile_common.cuh"
@@ -50,7 +51,7 @@ namespace {
 constexpr int kNT = 1024, kNW = kNT / 32;
 constexpr int kMaxD = 2048, kEPT = (kMaxD + kNT - 1) / kNT;  // log-likelihood elements per thread
 constexpr float kPostScale = 268435456.f;        // 2^28
-constexpr int kMaxItems = 64;                    // utterances per cluster
+constexpr int kMaxItems = kLptMaxItems;          // utterances per cluster
 // TMA slot ring (as fb_stream_kernel): 2 chunks of 8 slot rows per warp
 using Ring = SlotRing<2, 8, 64>;
 
@@ -129,50 +130,8 @@ __global__ void __launch_bounds__(kNT, 1)
   const bool negate = a.mode == kPostNegate;
 
   // ---- LPT assignment of the batch over the clusters (identical in every CTA) ----
-  {
-    int *lens = reinterpret_cast<int *>(vec);
-    int *order = lens + a.B;
-    for (int i = tid; i < a.B; i += kNT) lens[i] = item_frames(a.lengths, i, a.T_max);
-    __syncthreads();
-    for (int i = tid; i < a.B; i += kNT) {
-      const int ti = lens[i];
-      int r = 0;
-      for (int j = 0; j < a.B; ++j) {
-        const int tj = lens[j];
-        r += (tj > ti) | ((tj == ti) & (j < i));
-      }
-      order[r] = i;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      unsigned load[3] = {0u, 0u, 0u};
-      int cnt[3] = {0, 0, 0};
-      int mine = 0;
-      for (int r = 0; r < a.B; ++r) {
-        const int i = order[r];
-        unsigned key = 0xFFFFFFFFu;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const int bin = lane + 32 * q;
-          if (bin < nclusters && cnt[q] < kMaxItems) key = min(key, (load[q] << 7) | unsigned(bin));
-        }
-        const unsigned best = __reduce_min_sync(kFull, key);
-        const int bin = int(best & 127u);
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          if (lane + 32 * q == bin) {
-            load[q] += unsigned(lens[i] + 2);
-            ++cnt[q];
-          }
-        if (bin == cluster) {
-          if (lane == 0) items[4 + mine] = i;
-          ++mine;
-        }
-      }
-      if (lane == 0) items[0] = mine;
-    }
-    __syncthreads();
-  }
+  lpt_assign<kNT>(a.lengths, a.B, a.T_max, nclusters, cluster, 2, reinterpret_cast<int *>(vec),
+                  items);
   const int nitems = items[0];
   Ring ring;
   if constexpr (RING) {

@@ -1,9 +1,5 @@
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_full_size_parity.py -q -p no:cacheprovider -x > gpurun_out/t_par.log 2>&1; echo "rc=$?" >> gpurun_out/t_par.log
-timeout 600 python bench.py --steps 20 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_mono.log 2>&1
-timeout 600 python bench.py --config hmm --steps 20 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_hmm.log 2>&1
-LFMMI_OPTIONS=split_small=0 timeout 600 python bench.py --config hmm --steps 20 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_hmm16.log 2>&1
-timeout 600 python bench.py --config sweep --batch 128 --steps 10 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_sweep128.log 2>&1
-timeout 900 python bench.py --config sweep --steps 5 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_sweep.log 2>&1
-timeout 600 python scripts/host_overhead.py hmm wsj_mono > gpurun_out/host_overhead.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_hmm.csv python bench.py --config hmm --profile --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+for np in 0 136 142 146 148; do
+LFMMI_OPTIONS=tile_persist=$np timeout 900 python bench.py --config sweep --steps 5 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_sweep_np$np.log 2>&1
+done
+LFMMI_OPTIONS=tile_persist=142 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sweep142.csv python bench.py --config sweep --profile --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1

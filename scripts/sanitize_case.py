@@ -12,6 +12,7 @@ Cases pick the kernel under test with the library options (lfmmi_set_option):
   ring     fb_stream_kernel<1024,1> with its TMA slot ring (cp.async.bulk + mbarrier)
   ssplit   fb_streamsplit_kernel (forward | backward clusters, DSMEM scalars, kappa recursion)
            with its TMA slot ring; ssplit0 the same reading slot rows from L2
+  tilep    fb_tile_kernel<512> XDB as 2 persistent CTAs (in-kernel LPT, utterances back to back)
   hmm      phone-bigram den on fb_split_kernel with 8 lanes per state (xor-shuffle sums)
   numtile  numerators on the generic fb_tile_kernel<128> (linear kernel disabled)
 every case also runs the linear-chain numerator kernel (except numtile) and
@@ -41,6 +42,7 @@ CASES = {
     "ssplit": ("wsj_biphone", 3, dict(stream_mode="split")),
     "ssplit0": ("wsj_biphone", 3, dict(stream_mode="split", stream_ring=0)),
     "hmm": ("hmm", 3, dict()),
+    "tilep": ("wsj_mono", 3, dict(split=0, tile_persist=2)),
     "numtile": ("wsj_mono", 3, dict(linear=0)),
 }
 

@@ -124,7 +124,8 @@ def _kernel_env(kernel, lib_options):
     "smallden" (the small-graph threshold moved either way), "g2" / "g4s" (tile
     packs with 2 / 4 lanes per state on the tile / split kernels), "ssplit" /
     "ssplit0" (L2-resident graphs on the stream split kernel, with / without
-    the TMA slot ring)."""
+    the TMA slot ring), "tilep" (the den tile kernel as 2 persistent CTAs, several
+    utterances each)."""
     if kernel == "tile":  # one CTA per utterance (no forward/backward split)
         lib_options(split=0)
     if kernel in ("split1", "split2"):  # 2-CTA split, several utterances per cluster
@@ -144,6 +145,8 @@ def _kernel_env(kernel, lib_options):
         lib_options(tile_g=2, split=0)
     if kernel == "g4s":  # four lanes per state, split kernel
         lib_options(tile_g=4, split=1)
+    if kernel == "tilep":  # den tile kernel as 2 persistent CTAs over the in-kernel LPT
+        lib_options(split=0, tile_persist=2)
     if kernel == "ssplit":  # L2-resident graphs: forward | backward stream split (TMA ring)
         lib_options(stream_mode="split")
     if kernel == "ssplit0":  # ... slot rows straight from L2
@@ -152,7 +155,7 @@ def _kernel_env(kernel, lib_options):
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "noring",
                                     "group", "smallnum", "smallden", "g2", "g4s", "ssplit",
-                                    "ssplit0"])
+                                    "ssplit0", "tilep"])
 @pytest.mark.parametrize("config,batch_size", [("toy", None), ("wsj_mono", None), ("hmm", 24),
                                                ("wsj_biphone", 4), ("wsj_biphone", 100),
                                                ("sweep", 6)])

@@ -20,8 +20,8 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-CASES = ["split", "tile", "tile1x", "stream2", "stream1", "ring", "ssplit", "ssplit0", "hmm",
-         "numtile"]
+CASES = ["split", "tile", "tile1x", "tilep", "stream2", "stream1", "ring", "ssplit", "ssplit0",
+         "hmm", "numtile"]
 
 
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
