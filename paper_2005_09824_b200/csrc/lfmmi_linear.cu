@@ -433,6 +433,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   float *invs = lsm + 2 * lay.T4;   // (lsm + T4: row maxima slot, unused with E rows)   // backward normalisers n_t = 1 / inv_t at [t]
   float *Bh = invs + lay.T4 + 4;    // backward column B_h at the midpoint
   unsigned *hist = reinterpret_cast<unsigned *>(Bh + lay.SK) + wrole * lay.Dr;
+  const uint32_t hist32 = smem_u32(hist);
   float *ring = reinterpret_cast<float *>(Bh + lay.SK + 2 * lay.Dr) + wrole * kRing * lay.Dr;
   double *kap = reinterpret_cast<double *>(Bh + lay.SK + 2 * lay.Dr + 2 * kRing * lay.Dr);
   const int mode = a.mode;
@@ -649,8 +650,9 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
           const float a_p = (k ? (valid[k - 1] ? fmaf(r[k - 1], u, v) : 0.f) : fmaf(prev, u, vprev));
           const float gs = a_s * ws[k] * bcur[k] * zs;
           const float gi = a_p * wi[k] * bcur[k] * zs;
-          if (gs > 0.f) atomicAdd(hist + (pdp[k] & 0xffffu), __float2uint_rn(gs * kFix));
-          if (gi > 0.f) atomicAdd(hist + (pdp[k] >> 16), __float2uint_rn(gi * kFix));
+          // predicated REDs (no branch per term; zero / negative / NaN terms quantise to 0)
+          red_add_shared_nz(hist32 + ((pdp[k] & 0xffffu) << 2), __float2uint_rn(gs * kFix));
+          red_add_shared_nz(hist32 + ((pdp[k] >> 16) << 2), __float2uint_rn(gi * kFix));
         }
         __syncwarp();
         flush(t);
@@ -780,9 +782,9 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
                                      : (nvalid ? ynext + ld : 0.f);
           const float gs = al[k] * ws[k] * bs * zinv;
           const float go = al[k] * wo[k] * bn * zinv;
-          if (gs > 0.f) atomicAdd(hist + (pdp[k] & 0xffffu), __float2uint_rn(gs * kFix));
+          red_add_shared_nz(hist32 + ((pdp[k] & 0xffffu) << 2), __float2uint_rn(gs * kFix));
           const unsigned pdo = k + 1 < K ? (pdp[k + 1] >> 16) : pdo_last;
-          if (go > 0.f) atomicAdd(hist + pdo, __float2uint_rn(go * kFix));
+          red_add_shared_nz(hist32 + (pdo << 2), __float2uint_rn(go * kFix));
         }
         __syncwarp();
         flush(e);
