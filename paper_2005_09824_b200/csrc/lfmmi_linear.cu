@@ -430,7 +430,8 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   const int lane = threadIdx.x & 31, wrole = threadIdx.x >> 5;  // 0 forward, 1 backward
   const int D = a.D, T_max = a.T_max;
   float *scl = lsm;                 // forward scales (tot of column t+1 at [t])
-  float *invs = lsm + 2 * lay.T4;   // (lsm + T4: row maxima slot, unused with E rows)   // backward normalisers n_t = 1 / inv_t at [t]
+  float *invs = lsm + 2 * lay.T4;   // backward normalisers n_t = 1 / inv_t at [t]
+                                    // (lsm + T4: the row-maxima slot, unused with E rows)
   float *Bh = invs + lay.T4 + 4;    // backward column B_h at the midpoint
   unsigned *hist = reinterpret_cast<unsigned *>(Bh + lay.SK) + wrole * lay.Dr;
   const uint32_t hist32 = smem_u32(hist);
