@@ -51,7 +51,8 @@ const char *lfmmi_last_error(void);
  * Process-wide dispatch / debug options, one struct parsed once from the
  * LFMMI_OPTIONS environment variable ("name=value,...") and changeable here.
  * Names: tile, stream, linear (0/1: kernel families the dispatcher may use),
- * linear_split (numerators as forward | backward warps), emit (emissions
+ * linear_split (numerators as forward | backward warps), linear_k16w (warps
+ * per direction for numerators with S > 256: 2 or 1), emit (emissions
  * pre-pass), split (-1 auto / 0 off / 1 force), split_clusters (0 auto),
  * split_h64, tile_g (tile-pack lanes per state, 0 auto; pack time), stream_mode ("auto", "split", "1024x1", "1024x2", "512x2"),
  * stream_ring (TMA slot ring), num_group, tile_persist (den tile kernel with

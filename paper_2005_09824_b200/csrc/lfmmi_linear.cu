@@ -405,29 +405,44 @@ __device__ __forceinline__ void linear_item(const FBArgs<float> &a, float *lsm,
 // and the forward frame k >= h normalises by kappa_k / scale_{k-1}.  Emissions
 // from emit_kernel (PRE) only; K <= 8.
 struct LinSplitLayout {
-  int T4, Dr, SK;
+  int T4, Dr, SK, nwd;
   size_t bytes;
 };
 
-__host__ __device__ inline LinSplitLayout lin_split_layout(int T_max, int D, int K) {
+// nwd: warps per direction (1, or 2 for the K = 16 class: 64 lanes x 8 states).
+__host__ __device__ inline LinSplitLayout lin_split_layout(int T_max, int D, int K, int nwd = 1) {
   LinSplitLayout l;
   l.T4 = pad4(T_max);
   l.Dr = pad4(D);
   l.SK = 32 * K;
-  // scales | shifts | inv (T4 + 4) | B_h (32 K) | hist[2][Dr] | ring[2][kRing][Dr] | kappa (2 doubles)
-  l.bytes = size_t(3 * l.T4 + 4 + l.SK + 2 * l.Dr + 2 * kRing * l.Dr) * 4 + 32;
+  l.nwd = nwd;
+  // scales | shifts | inv (T4 + 4) | B_h (32 K) | hist[2][Dr] | ring[2 nwd][kRing][Dr] |
+  // kappa + partials (4 doubles) | exchange slots (32 floats)
+  l.bytes = size_t(3 * l.T4 + 4 + l.SK + 2 * l.Dr + 2 * nwd * kRing * l.Dr) * 4 + 32 + 128;
   return l;
 }
 
-// The two warps of a split utterance meet at different code locations (the
-// forward warp inside its frame loop, the backward warp at its midpoint), so
-// they use the non-aligned named barrier 1 (64 threads), not __syncthreads.
-__device__ __forceinline__ void pair_sync() { asm volatile("barrier.sync 1, 64;\n" ::: "memory"); }
+// The two directions of a split utterance meet at different code locations (the
+// forward warps inside their frame loop, the backward warps at their midpoint),
+// so they use the non-aligned named barrier 1 (all 64 NWD threads), not
+// __syncthreads; the two warps of one direction (NWD = 2) use barrier 2 / 3.
+template <int NWD>
+__device__ __forceinline__ void pair_sync() {
+  asm volatile("barrier.sync 1, %0;\n" ::"n"(64 * NWD) : "memory");
+}
 
-template <int K>
+// NWD = 1: one warp per direction, lane l owns states [l K, l K + K).  NWD = 2
+// (the K = 16 class as 64 lanes x 8 states): the two warps of a direction
+// exchange the column sum and the boundary state through shared memory once
+// per frame (one 64-thread named barrier), share the posterior bins, and split
+// the gradient-row flush.
+template <int K, int NWD = 1>
 __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float *lsm,
                                                   const LinSplitLayout &lay, int b) {
-  const int lane = threadIdx.x & 31, wrole = threadIdx.x >> 5;  // 0 forward, 1 backward
+  constexpr int NG = 32 * NWD;  // lanes per direction
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wrole = warp / NWD, half = warp % NWD;  // 0 forward, 1 backward; warp within it
+  const int gl = half * 32 + lane;                  // lane within the direction
   const int D = a.D, T_max = a.T_max;
   float *scl = lsm;                 // forward scales (tot of column t+1 at [t])
   float *invs = lsm + 2 * lay.T4;   // backward normalisers n_t = 1 / inv_t at [t]
@@ -435,8 +450,26 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   float *Bh = invs + lay.T4 + 4;    // backward column B_h at the midpoint
   unsigned *hist = reinterpret_cast<unsigned *>(Bh + lay.SK) + wrole * lay.Dr;
   const uint32_t hist32 = smem_u32(hist);
-  float *ring = reinterpret_cast<float *>(Bh + lay.SK + 2 * lay.Dr) + wrole * kRing * lay.Dr;
-  double *kap = reinterpret_cast<double *>(Bh + lay.SK + 2 * lay.Dr + 2 * kRing * lay.Dr);
+  float *ring = reinterpret_cast<float *>(Bh + lay.SK + 2 * lay.Dr) + warp * kRing * lay.Dr;
+  double *kap = reinterpret_cast<double *>(Bh + lay.SK + 2 * lay.Dr + 2 * NWD * kRing * lay.Dr);
+  // exchange slots (NWD = 2): [wrole][frame parity][4] | [wrole][2] | boundary arcs [wrole][2]
+  float *xch = reinterpret_cast<float *>(kap + 4);
+  auto group_sync = [&]() {
+    if constexpr (NWD == 1)
+      __syncwarp();
+    else
+      asm volatile("barrier.sync %0, 64;\n" ::"r"(2 + wrole) : "memory");
+  };
+  // sum over the direction's lanes (identical in every lane); slot: 2 floats
+  auto group_sum = [&](float v, float *slot) {
+    v = warp_sum(v);
+    if constexpr (NWD > 1) {
+      if (lane == 0) slot[half] = v;
+      group_sync();
+      v = slot[0] + slot[1];
+    }
+    return v;
+  };
   const int mode = a.mode;
   const bool reads_post = mode == kPostAdd || mode == kPostSubtract;
 
@@ -449,21 +482,21 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   const float *Emb = a.Em + row0;
   float *post_b = a.post + row0 * D;
   if (wrole == 0 && !reads_post && !a.packed)
-    for (size_t i = lane; i < size_t(T_max - T) * D; i += 32) post_b[size_t(T) * D + i] = 0.f;
+    for (size_t i = gl; i < size_t(T_max - T) * D; i += NG) post_b[size_t(T) * D + i] = 0.f;
   if (T <= 0) {
     if (wrole == 0) {
       if (a.scale_logs && !a.packed)
-        for (int k = lane; k < T_max; k += 32) a.scale_logs[size_t(b) * T_max + k] = 0.0;
-      if (lane == 0) {
+        for (int k = gl; k < T_max; k += NG) a.scale_logs[size_t(b) * T_max + k] = 0.0;
+      if (gl == 0) {
         a.logp[b] = NAN;
         a.fail[b] = 0;
       }
     }
-    return;  // both warps: no barriers for this item
+    return;  // every warp: no barriers for this item
   }
   const int ldt = (a.S_max + 31) & ~31;
   float *tr = a.work + size_t(off) * ldt;
-  const bool own_row = lane * K < ldt;
+  const bool own_row = gl * K < ldt;
   const int h = T == 1 ? 1 : min(T - 1, max(1, (T * 33 + 32) >> 6));
 
   const int4 item = a.g.lin_item[a.row_map[b]];
@@ -474,7 +507,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   bool valid[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const int s = lane * K + k;
+    const int s = gl * K + k;
     valid[k] = s < S;
     const uint4 v = valid[k] ? rec[s] : make_uint4(0u, 0u, 0u, 0u);
     ps[k] = __uint_as_float(v.x);
@@ -484,7 +517,19 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   }
   float po_last = __shfl_down_sync(kFull, pin[0], 1);
   unsigned pdo_last = __shfl_down_sync(kFull, pdp[0], 1) >> 16;
-  if (lane == 31) {
+  if constexpr (NWD > 1) {  // the first state of the next warp of this direction
+    float *xb = xch + 24 + 2 * wrole;
+    if (half == 1 && lane == 0) {
+      xb[0] = pin[0];
+      xb[1] = __uint_as_float(pdp[0] >> 16);
+    }
+    group_sync();
+    if (half == 0 && lane == 31) {
+      po_last = xb[0];
+      pdo_last = __float_as_uint(xb[1]);
+    }
+  }
+  if (gl == NG - 1) {
     po_last = 0.f;
     pdo_last = 0u;
   }
@@ -505,7 +550,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = 0.f;
     if (!own_row || t < 0 || t >= T) return;
-    const float *src = tr + size_t(t) * ldt + lane * K;
+    const float *src = tr + size_t(t) * ldt + gl * K;
     if constexpr (K >= 4) {
 #pragma unroll
       for (int c = 0; c < K; c += 4) {
@@ -522,7 +567,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
   };
   auto store_row_k = [&](int t, const float *v) {
     if (!own_row) return;
-    float *dst = tr + size_t(t) * ldt + lane * K;
+    float *dst = tr + size_t(t) * ldt + gl * K;
     if constexpr (K >= 4) {
 #pragma unroll
       for (int c = 0; c < K; c += 4)
@@ -538,7 +583,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
     if (vflush) {
       uint4 *h4 = reinterpret_cast<uint4 *>(hist);
       float4 *p4 = reinterpret_cast<float4 *>(prow);
-      for (int c = lane; c < (D >> 2); c += 32) {
+      for (int c = gl; c < (D >> 2); c += NG) {
         const uint4 hv = h4[c];
         h4[c] = make_uint4(0u, 0u, 0u, 0u);
         float4 g = make_float4(float(hv.x) * kUnfix, float(hv.y) * kUnfix, float(hv.z) * kUnfix,
@@ -553,7 +598,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         p4[c] = g;
       }
     } else {
-      for (int d = lane; d < D; d += 32) {
+      for (int d = gl; d < D; d += NG) {
         float g = float(hist[d]) * kUnfix;
         hist[d] = 0u;
         if (mode == kPostNegate) g = -g;
@@ -563,14 +608,14 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       }
     }
   };
-  for (int d = lane; d < lay.Dr; d += 32) hist[d] = 0u;
+  for (int d = gl; d < lay.Dr; d += NG) hist[d] = 0u;
   const bool other_failed = a.other_fail != nullptr && a.other_fail[b] >= 0;
 
   if (wrole == 0) {
     // ======================= forward warp =========================================
     float r[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) r[k] = (lane * K + k == init) ? 1.f : 0.f;
+    for (int k = 0; k < K; ++k) r[k] = (gl * K + k == init) ? 1.f : 0.f;
     int fail_at = -1;
     bool mid_done = false;
     double kappa = 0.0;
@@ -578,16 +623,21 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
 #pragma unroll
     for (int k = 0; k < K; ++k) bcur[k] = 0.f;
     auto midpoint = [&](const float *raw) {  // kappa_h = sum raw_h B_h
-      pair_sync();  // B_h, backward rows >= h and inv_t are written
+      pair_sync<NWD>();  // B_h, backward rows >= h and inv_t are written
       double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k)
-        if (valid[k]) acc += double(raw[k]) * double(Bh[lane * K + k]);
+        if (valid[k]) acc += double(raw[k]) * double(Bh[gl * K + k]);
       acc = warp_sum(acc);
-      if (lane == 0) kap[0] = acc;
+      if constexpr (NWD > 1) {
+        if (lane == 0) kap[2 + half] = acc;
+        group_sync();
+        acc = kap[2] + kap[3];
+      }
+      if (gl == 0) kap[0] = acc;
       kappa = acc;
       mid_done = true;
-      pair_sync();  // kappa_h delivered
+      pair_sync<NWD>();  // kappa_h delivered
     };
 #pragma unroll
     for (int p = 0; p < kRing - 1; ++p) {
@@ -609,8 +659,15 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
 #pragma unroll
       for (int k = 0; k < K; ++k) R += r[k];
       float prev = __shfl_up_sync(kFull, r[K - 1], 1);
-      if (lane == 0) prev = 0.f;
-      R = warp_sum(R);
+      {
+        float *x = xch + (wrole * 2 + (t & 1)) * 4;
+        if constexpr (NWD > 1)
+          if (half == 0 && lane == 31) x[2] = r[K - 1];  // published by the group_sum barrier
+        R = group_sum(R, x);
+        if constexpr (NWD > 1)
+          if (half == 1 && lane == 0) prev = x[2];
+      }
+      if (gl == 0) prev = 0.f;
       float ws[K], wi[K], A[K], Bv[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -631,7 +688,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
           break;
         }
         u = rcp_rn(tot);
-        if (lane == 0) scl[t - 1] = tot;
+        if (gl == 0) scl[t - 1] = tot;
       }
       if (t < h) {  // alpha_t for the backward warp's posteriors
         float al[K];
@@ -644,7 +701,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         // backward normaliser n_{t+1} = 1 / inv_{t+1} are at hand)
         const double zt = kappa * double(u);
         const float zs = (zt > 1e-37 && zt < 1e37) ? __frcp_rn(float(zt)) : 0.f;
-        const float vprev = (lane * K > 0 && lane * K - 1 < S) ? v : 0.f;
+        const float vprev = (gl * K > 0 && gl * K - 1 < S) ? v : 0.f;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const float a_s = valid[k] ? fmaf(r[k], u, v) : 0.f;
@@ -655,9 +712,9 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
           red_add_shared_nz(hist32 + ((pdp[k] & 0xffffu) << 2), __float2uint_rn(gs * kFix));
           red_add_shared_nz(hist32 + ((pdp[k] >> 16) << 2), __float2uint_rn(gi * kFix));
         }
-        __syncwarp();
+        group_sync();  // every warp's bins of frame t are in
         flush(t);
-        __syncwarp();
+        __syncwarp();  // (the next frame's group_sum barrier orders the clears)
         kappa = zt * double(invs[t + 1]);  // kappa_{t+1} = Z_t / inv_{t+1} (invs holds n = 1 / inv)
         if (t + 1 < T) load_row_k(t + 1, bcur);
       }
@@ -673,23 +730,23 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       float R = 0.f;
 #pragma unroll
       for (int k = 0; k < K; ++k) R += r[k];
-      R = warp_sum(R);
+      R = group_sum(R, xch + 16 + 2 * wrole);
       const float tot = (leak > 0.f && R > 0.f) ? R + leak * R : R;
       if (!(tot >= a.floor_eff) || tot == INFINITY)
         fail_at = T - 1;
-      else if (lane == 0)
+      else if (gl == 0)
         scl[T - 1] = tot;
     }
     if (!mid_done) {  // T == 1 (kappa_1 = scale_0) or failed before the midpoint
       __syncwarp();
-      pair_sync();
-      if (lane == 0) kap[0] = fail_at < 0 ? double(scl[T - 1]) : 1.0;
-      pair_sync();
+      pair_sync<NWD>();
+      if (gl == 0) kap[0] = fail_at < 0 ? double(scl[T - 1]) : 1.0;
+      pair_sync<NWD>();
     }
-    if (fail_at >= 0 && lane == 0)
+    if (fail_at >= 0 && gl == 0)
       for (int k = fail_at; k < T; ++k) scl[k] = 1.f;
-    pair_sync();  // end: the backward warp's posterior rows are written
-    {
+    pair_sync<NWD>();  // end: the backward warps' posterior rows (and scl) are written
+    if (half == 0) {
       double acc = 0.0;
       for (int k = lane; k < T; k += 32) {
         const double val = log(double(scl[k])) + double(Emb[k]);
@@ -705,7 +762,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       }
     }
     if (fail_at >= 0 || other_failed)
-      for (size_t i = lane; i < size_t(T) * D; i += 32) post_b[i] = 0.f;
+      for (size_t i = gl; i < size_t(T) * D; i += NG) post_b[i] = 0.f;
   } else {
     // ======================= backward warp ========================================
     float Y[K];  // pre-leak column t in this warp's own scale; B_t = Y + ld_t
@@ -731,13 +788,13 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         float sY = 0.f;
 #pragma unroll
         for (int k = 0; k < K; ++k) sY += Y[k];
-        sY = warp_sum(sY);
+        sY = group_sum(sY, xch + 16 + 2 * wrole);
         const float ldh = (t < T && leak > 0.f) ? leak * sY / float(S) : 0.f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) Bh[lane * K + k] = valid[k] ? Y[k] + ldh : 0.f;
+        for (int k = 0; k < K; ++k) Bh[gl * K + k] = valid[k] ? Y[k] + ldh : 0.f;
         __threadfence_block();
-        pair_sync();  // forward warp computes kappa_h
-        pair_sync();
+        pair_sync<NWD>();  // forward warps compute kappa_h
+        pair_sync<NWD>();
         kappa = kap[0];
         load_row_k(e, al);
       }
@@ -749,7 +806,15 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
 #pragma unroll
       for (int k = 0; k < K; ++k) sY += Y[k];
       float ynext = __shfl_down_sync(kFull, Y[0], 1);
-      if (lane == 31) ynext = 0.f;
+      {
+        float *xf = xch + (wrole * 2 + (t & 1)) * 4;
+        if constexpr (NWD > 1)
+          if (half == 1 && lane == 0) xf[2] = Y[0];  // published by the group_sum barrier
+        sY = group_sum(sY, xf);
+        if constexpr (NWD > 1)
+          if (half == 0 && lane == 31) ynext = xf[2];
+      }
+      if (gl == NG - 1) ynext = 0.f;
       float ws[K], wo[K], A[K], Bv[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) ws[k] = ps[k] * Lt[pdp[k] & 0xffffu];
@@ -761,11 +826,10 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         A[k] = ws[k] * Y[k] + wo[k] * (k + 1 < K ? Y[k + 1] : ynext);
         Bv[k] = ws[k] + wo[k];
       }
-      sY = warp_sum(sY);
       const float ld = (t < T && leak > 0.f) ? leak * sY / float(S) : 0.f;
       const float n = sY + ld * float(S);
       const float inv = (n > 0.f && n < INFINITY) ? rcp_rn(n) : 1.f;
-      if (lane == 0) invs[t] = (n > 0.f && n < INFINITY) ? n : 1.f;  // n_t = 1 / inv_t
+      if (gl == 0) invs[t] = (n > 0.f && n < INFINITY) ? n : 1.f;  // n_t = 1 / inv_t
       if (!post) {  // beta'_t = B_t inv_t -> row e (the forward warp's posteriors)
         if (t > h) {
           float bb[K];
@@ -775,7 +839,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
         }
       } else {  // posteriors of frame e: alpha_e p e B_t / kappa_t
         const float zinv = (kappa > 1e-37 && kappa < 1e37) ? __frcp_rn(float(kappa)) : 0.f;
-        const bool nvalid = lane * K + K < S;  // state lane K + K exists
+        const bool nvalid = gl * K + K < S;  // state gl K + K exists
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const float bs = valid[k] ? Y[k] + ld : 0.f;
@@ -787,9 +851,9 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
           const unsigned pdo = k + 1 < K ? (pdp[k + 1] >> 16) : pdo_last;
           red_add_shared_nz(hist32 + (pdo << 2), __float2uint_rn(go * kFix));
         }
-        __syncwarp();
+        group_sync();  // every warp's bins of frame e are in
         flush(e);
-        __syncwarp();
+        __syncwarp();  // (the next frame's group_sum barrier orders the clears)
         if (t >= 2) kappa = double(inv) * kappa * double(scl[t - 2]);  // kappa_{t-1}
         load_row_k(e - 1, al);
       }
@@ -797,7 +861,7 @@ __device__ __forceinline__ void linear_item_split(const FBArgs<float> &a, float 
       for (int k = 0; k < K; ++k) Y[k] = inv * fmaf(ld, Bv[k], A[k]);
     }
     cp_async_wait<0>();
-    pair_sync();  // end
+    pair_sync<NWD>();  // end
   }
 }
 
@@ -838,6 +902,32 @@ __global__ void __launch_bounds__(64) fb_linear_split_kernel(const FBArgs<float>
     case 8: if constexpr (KLO <= 8 && KHI >= 8) linear_item_split<8>(a, lsm, lay, b); break;
     default: if constexpr (KHI >= 16) linear_item_split<16>(a, lsm, lay, b); break;
   }
+}
+
+// The K = 16 class (S in (256, 512]) as two warps per direction (64 lanes x 8
+// states, 128 threads): half the per-lane chain of the one-warp K = 16 variant
+// (254 registers), one 64-thread barrier per frame for the column sum and the
+// warp-boundary state.
+__global__ void __launch_bounds__(128) fb_linear_split2_kernel(const FBArgs<float> a, int kstage) {
+  extern __shared__ __align__(16) float lsm[];
+  const int b = blockIdx.x;
+  if (k_of(a.g.lin_item[a.row_map[b]].y) != 16) return;
+  const LinSplitLayout lay = lin_split_layout(a.T_max, a.D, kstage, 2);
+  linear_item_split<8, 2>(a, lsm, lay, b);
+}
+
+int launch_split2(const FBArgs<float> &a, int ks, cudaStream_t st) {
+  const size_t ssm = lin_split_layout(a.T_max, a.D, ks, 2).bytes;
+  if (ssm > size_t(kMaxSmem)) return LFMMI_ERR_UNSUPPORTED;
+  if (ssm > 48 * 1024) {
+    const int rc = check_cuda(cudaFuncSetAttribute(fb_linear_split2_kernel,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(ssm)),
+                              "cudaFuncSetAttribute(linear split2)");
+    if (rc) return rc;
+  }
+  fb_linear_split2_kernel<<<a.B, 128, ssm, st>>>(a, ks);
+  return check_cuda(cudaGetLastError(), "fb_linear_split2_kernel launch");
 }
 
 template <int KLO, int KHI>
@@ -890,6 +980,10 @@ int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st
                : kstage == 4 ? launch_split_k<1, 4>(a, kstage, ssm, st)
                              : launch_split_k<1, 8>(a, kstage, ssm, st);
       if (rc || kstage <= 8) return rc;
+      if (options().linear_k16w == 2) {
+        const int rc2 = launch_split2(a, kstage, st);
+        if (rc2 != LFMMI_ERR_UNSUPPORTED) return rc2;
+      }
       return launch_split_k<16, 16>(a, kstage, ssm, st);
     }
   }

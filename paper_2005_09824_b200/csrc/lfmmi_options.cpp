@@ -23,6 +23,7 @@ const Field kFields[] = {
     {"linear", &Options::linear, nullptr},
     {"linear_split", &Options::linear_split, nullptr},
     {"linear_k16", &Options::linear_k16, nullptr},
+    {"linear_k16w", &Options::linear_k16w, nullptr},
     {"split", &Options::split, nullptr},
     {"split_clusters", &Options::split_clusters, nullptr},
     {"split_h64", &Options::split_h64, nullptr},

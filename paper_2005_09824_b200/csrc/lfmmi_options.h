@@ -14,6 +14,7 @@ struct Options {
   int stream = 1;         // L2-streamed kernel (graphs beyond shared memory)
   int linear = 1;         // linear-chain numerator kernel
   int linear_split = 1;   // ... with forward | backward warps (chain loss, fp32)
+  int linear_k16w = 2;    // ... the K = 16 class: warps per direction (2: 64 lanes x 8 states, 1: one warp)
   int linear_k16 = 0;     // ... batches with S > 256: 1 = one launch for every K, 0 = K <= 8 then K = 16
   int split = -1;         // denominator split kernel: -1 auto (B <= 2 x SMs), 0 off, 1 force
   int split_clusters = 0; // 0 = auto

@@ -12,6 +12,8 @@ Cases pick the kernel under test with the library options (lfmmi_set_option):
   ring     fb_stream_kernel<1024,1> with its TMA slot ring (cp.async.bulk + mbarrier)
   ssplit   fb_streamsplit_kernel (forward | backward clusters, DSMEM scalars, kappa recursion)
            with its TMA slot ring; ssplit0 the same reading slot rows from L2
+  lin16    numerators with S > 256 on the two-warps-per-direction linear kernel (one 900-frame
+           utterance; racecheck over the 64-thread exchange barriers)
   tilep    fb_tile_kernel<512> XDB as 2 persistent CTAs (in-kernel LPT, utterances back to back)
   hmm      phone-bigram den on fb_split_kernel with 8 lanes per state (xor-shuffle sums)
   numtile  numerators on the generic fb_tile_kernel<128> (linear kernel disabled)
@@ -43,6 +45,7 @@ CASES = {
     "ssplit0": ("wsj_biphone", 3, dict(stream_mode="split", stream_ring=0)),
     "hmm": ("hmm", 3, dict()),
     "tilep": ("wsj_mono", 3, dict(split=0, tile_persist=2)),
+    "lin16": ("wsj_mono", 2, dict()),
     "numtile": ("wsj_mono", 3, dict(linear=0)),
 }
 
@@ -56,7 +59,7 @@ def main(case):
         ext.set_option(k, str(v))
     w = synth.make_workload(config, seed=2, batch_size=B)
     rng = np.random.default_rng(1)
-    T = [24, 17, 9][:B]
+    T = [24, 17, 9][:B] if case != "lin16" else [900, 12]
     w.seqs = [s[:t] for s, t in zip(w.seqs, T)]
     w.lengths = np.asarray(T, dtype=np.int64)
     w.num_phones = [rng.integers(0, w.D // 2, max(1, t // 3)).tolist() for t in T]

@@ -232,3 +232,27 @@ def test_linear_split_bitwise_batch_independent(cuda):
     offs = np.concatenate([[0], np.cumsum([len(q) for q in seqs])])
     assert ns[0] == nf[3] and ns[1] == nf[7]
     np.testing.assert_array_equal(gs[:len(seqs[3])], gf[offs[3]:offs[4]])
+
+
+@pytest.mark.parametrize("k16w", [2, 1])
+@pytest.mark.parametrize("leak", [1e-5, 0.1])
+def test_linear_k16_class_vs_oracle(cuda, lib_options, k16w, leak):
+    """Numerators with S > 256 (the K = 16 class, sweep's long utterances): two
+    warps per direction (64 lanes x 8 states, the default) or one (32 x 16),
+    next to K <= 8 utterances in the same batch."""
+    lib_options(linear_k16w=k16w)
+    w = synth.make_workload("sweep", seed=5, batch_size=6)
+    rng = np.random.default_rng(17)
+    T = [1500, 1210, 800, 300, 905, 61]
+    w.seqs = [rng.normal(0.0, 2.0, size=(t, w.D)).astype(np.float32).astype(np.float64) for t in T]
+    w.lengths = np.asarray(T, dtype=np.int64)
+    w.num_phones = [rng.integers(0, w.D // 2, max(1, t // 3)).tolist() for t in T]
+    batch, nums, den = w.build(P)
+    assert nums.max_states > 256
+    opts = P.FBOptions(leak_coefficient=leak)
+    res = P.chain_loss(batch, nums, den, opts)
+    ref = O.chain_loss(batch, nums, den, leak=leak)
+    assert abs(res.objective - ref.objective) <= 1e-5 * max(1.0, abs(ref.objective))
+    assert np.abs(res.grad - ref.grad).max() <= GRAD_ABS
+    for (a, _), (c, _) in zip(res.per_utt, ref.per_utt):
+        assert abs(a - c) <= 1e-5 * max(1.0, abs(c))

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 CASES = ["split", "tile", "tile1x", "tilep", "stream2", "stream1", "ring", "ssplit", "ssplit0",
-         "hmm", "numtile"]
+         "hmm", "numtile", "lin16"]
 
 
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
