@@ -50,17 +50,25 @@ const char *lfmmi_last_error(void);
 /*
  * Process-wide dispatch / debug options, one struct parsed once from the
  * LFMMI_OPTIONS environment variable ("name=value,...") and changeable here.
- * Names: tile, stream, linear (0/1: kernel families the dispatcher may use),
- * linear_split (numerators as forward | backward warps), linear_k16w (warps
- * per direction for numerators with S > 256: 2 or 1), emit (emissions
- * pre-pass), split (-1 auto / 0 off / 1 force), split_clusters (0 auto),
- * split_h64, tile_g (tile-pack lanes per state, 0 auto; pack time), stream_mode ("auto", "split", "1024x1", "1024x2", "512x2"),
- * stream_ring (TMA slot ring), num_group, tile_persist (den tile kernel with
- * more utterances than SMs: persistent CTAs over an in-kernel LPT), small_arcs (graphs with <= 512
- * states and <= small_arcs arcs take the numerator-sized kernels), tile_xdb,
- * serial (-1 auto / 0 / 1:
- * numerator pass before the denominator pass), sched_iters (-1 auto),
- * chore_bias (pack time), debug, profile ("", "split", "tile").
+ * Names:
+ *   tile, stream, linear   0/1: kernel families the dispatcher may use
+ *   linear_split           numerators as forward | backward warps
+ *   linear_k16w            warps per direction for numerators with S > 256 (2 or 1)
+ *   linear_k16             1: one numerator launch for every K
+ *   emit                   emissions pre-pass of the chain loss
+ *   split                  den split kernel: -1 auto / 0 off / 1 force
+ *   split_clusters, split_h64   cluster count (0 auto), midpoint in 64ths of T
+ *   small_arcs, small_indeg     graphs with <= 512 states, <= small_arcs arcs and
+ *                          in-degree <= small_indeg take the numerator-sized kernels
+ *   tile_g                 tile-pack lanes per state (0 auto; pack time)
+ *   tile_xdb, tile_persist den tile kernel: double-buffered slots; persistent CTAs
+ *                          over an in-kernel LPT when B > SMs (0 off, 1 auto, >= 2 force)
+ *   stream_mode            "auto", "split", "1024x1", "1024x2", "512x2"
+ *   stream_ring            TMA slot ring of the stream kernels
+ *   num_group              threads per utterance of the generic numerator kernel
+ *   serial                 -1 auto / 0 / 1: numerator pass before the den pass
+ *   sched_iters, chore_bias     pack-time scheduling knobs
+ *   debug, profile         stderr notes; "", "split", "tile" cycle counters
  * Unknown names return LFMMI_ERR_INVALID.  Not thread-safe against
  * concurrent launches: set them before use.
  */

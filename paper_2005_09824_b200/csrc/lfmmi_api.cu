@@ -276,12 +276,14 @@ int run_fused(const lfmmi_graphs *graphs, const int64_t *row_map, int B, int T_m
   }
   if (work_bytes < size_t(a.S_pad) * sizeof(Real))
     return set_error(LFMMI_ERR_INVALID, "workspace too small");
-  // Numerator-sized graphs: a warp group per utterance.  Larger or denser
-  // graphs (a 43-state phone-bigram den has ~1850 arcs): the den kernels.  The
-  // choice depends only on the graph batch, so an utterance's result never
-  // depends on which other utterances share its batch.
+  // Numerator-sized graphs (chains and thin lattices: few states, in-degree
+  // <= 4): a warp group per utterance.  Larger or denser graphs — a 43-state
+  // phone-bigram den (~1850 arcs), the 50-state toy den (in-degree up to 10) —
+  // take the den kernels (forward | backward split: toy step 0.156 -> 0.069 ms).
+  // The choice depends only on the graph batch's shape.
   const Options &opt = options();
-  const bool small = graphs->max_states <= 512 && graphs->max_arcs <= opt.small_arcs;
+  const bool small = graphs->max_states <= 512 && graphs->max_arcs <= opt.small_arcs &&
+                     graphs->max_in_deg <= opt.small_indeg;
   if constexpr (std::is_same<Real, float>::value) {
     if (graphs->linear && opt.linear) {  // the reference's numerators: linear chains
       const int rc = launch_linear(a, graphs, st);

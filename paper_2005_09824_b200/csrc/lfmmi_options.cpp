@@ -31,6 +31,7 @@ const Field kFields[] = {
     {"stream_ring", &Options::stream_ring, nullptr},
     {"num_group", &Options::num_group, nullptr},
     {"small_arcs", &Options::small_arcs, nullptr},
+    {"small_indeg", &Options::small_indeg, nullptr},
     {"tile_xdb", &Options::tile_xdb, nullptr},
     {"tile_persist", &Options::tile_persist, nullptr},
     {"serial", &Options::serial, nullptr},

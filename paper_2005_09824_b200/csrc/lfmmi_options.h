@@ -22,8 +22,8 @@ struct Options {
   std::string stream_mode = "auto";  // "auto" | "1024x1" | "1024x2" | "512x2"
   int stream_ring = 1;    // stream kernel: TMA slot ring when it fits (biphone 9.45 vs 9.96 ms)
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
-  int small_arcs = 1024;  // graphs with <= 512 states AND <= this many arcs per row take the
-                          // numerator-sized kernels; denser ones (a phone-bigram den) the den path
+  int small_arcs = 1024;  // graphs with <= 512 states, <= this many arcs per row AND in-degree
+  int small_indeg = 4;    // <= small_indeg take the numerator-sized kernels; denser ones the den path
   int tile_persist = 0;  // den tile kernel, B > SMs: persistent CTAs over an in-kernel LPT
                          // (0 off, >= 2: force that many CTAs — tests)
   int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots

@@ -138,7 +138,7 @@ def _kernel_env(kernel, lib_options):
     if kernel == "noring":  # stream kernel reading slot rows straight from L2 (no TMA ring)
         lib_options(stream_ring=0, stream_mode="1024x1")
     if kernel == "smallnum":  # every graph <= 512 states (the hmm den too) numerator-sized
-        lib_options(small_arcs=1 << 30)
+        lib_options(small_arcs=1 << 30, small_indeg=1 << 30)
     if kernel == "smallden":  # every graph on the den kernels (numerators too)
         lib_options(small_arcs=0, linear=0)
     if kernel == "g2":  # tile packs with two lanes per state (pack time), tile kernel
