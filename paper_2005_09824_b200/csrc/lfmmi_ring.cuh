@@ -22,11 +22,14 @@ template <int NSLOT, int ROWS, int CHUNKS>
 struct SlotRing {
   static_assert(ROWS >= 1 && NSLOT >= 1, "ring shape");
   static constexpr unsigned kSlotBytes = unsigned(ROWS) * 256u;
+  // (32-bit shared addresses and no cached lane id: the 1024-thread kernels
+  // using the ring run under a 64-register cap)
   uint32_t ring32 = 0, bars32 = 0;  // this warp's slots / mbarriers
-  uint2 *ctab = nullptr;            // this warp's chunk table (CHUNKS entries)
+  uint32_t ctab32 = 0;              // this warp's chunk table (CHUNKS x {offset, bytes})
   const uint2 *pack = nullptr;
   unsigned g_cons = 0, g_iss = 0, g_end = 0;  // chunks consumed / issued / phase end
-  int p_i = 0, nchunk = 0, lane = 0;
+  int p_i = 0, nchunk = 0;
+  __device__ __forceinline__ static int lane_id() { return int(threadIdx.x & 31u); }
 
   // Shared bytes for NW warps: slots, barriers, chunk tables.
   __host__ __device__ static constexpr unsigned slot_bytes(int nw) {
@@ -40,11 +43,10 @@ struct SlotRing {
   }
 
   __device__ __forceinline__ void init(unsigned char *slots, unsigned char *bars,
-                                       unsigned char *tables, int warp, int lane_) {
+                                       unsigned char *tables, int warp) {
     ring32 = smem_u32(slots) + unsigned(warp) * (NSLOT * kSlotBytes);
     bars32 = smem_u32(bars) + unsigned(warp) * (NSLOT * 8u);
-    ctab = reinterpret_cast<uint2 *>(tables) + size_t(warp) * CHUNKS;
-    lane = lane_;
+    ctab32 = smem_u32(tables) + unsigned(warp) * (CHUNKS * 8u);
   }
   // Once per CTA before first use (then a CTA barrier): one arrival per phase.
   __device__ static void init_barriers(unsigned char *bars, int nw, int tid) {
@@ -57,8 +59,8 @@ struct SlotRing {
   __device__ __forceinline__ uint32_t bar(unsigned g) const { return bars32 + (g % NSLOT) * 8u; }
 
   __device__ __forceinline__ void issue() {
-    if (lane == 0) {
-      const uint2 ent = ctab[p_i];
+    if (lane_id() == 0) {
+      const uint2 ent = lds_v2(ctab32 + unsigned(p_i) * 8u);
       fence_proxy_async_smem();  // earlier LDS of this slot before the async refill
       bulk_copy_g2s(slot(g_iss), pack + ent.x, ent.y, bar(g_iss));
     }
@@ -78,8 +80,9 @@ struct SlotRing {
       const int tr = __shfl_sync(kFull, my_trips, i);
       const int bs = __shfl_sync(kFull, my_base, i);
       for (int j0 = 0; j0 < tr; j0 += ROWS, ++c)
-        if (lane == 0 && c < CHUNKS)
-          ctab[c] = make_uint2(unsigned(bs + 32 * j0), unsigned(min(ROWS, tr - j0)) * 256u);
+        if (lane_id() == 0 && c < CHUNKS)
+          sts_v2(ctab32 + unsigned(c) * 8u,
+                 make_uint2(unsigned(bs + 32 * j0), unsigned(min(ROWS, tr - j0)) * 256u));
     }
     if (c > CHUNKS) __trap();  // launcher bug: the table cannot hold this warp's chunks
     nchunk = c;
@@ -99,7 +102,7 @@ struct SlotRing {
   __device__ __forceinline__ void rows(int trips, Body &&body) {
     for (int j0 = 0; j0 < trips; j0 += ROWS) {
       mbar_wait(bar(g_cons), (g_cons / NSLOT) & 1u);
-      const uint32_t sl = slot(g_cons) + unsigned(lane) * 8u;
+      const uint32_t sl = slot(g_cons) + unsigned(lane_id()) * 8u;
       const int n = min(ROWS, trips - j0);
       // two halves: the first half's arc bodies run while the second half's
       // words are loaded, with half the word registers live (the 1024-thread

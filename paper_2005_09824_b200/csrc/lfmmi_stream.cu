@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     }
   };
   if constexpr (RING) {
-    ring.init(smem + lay.ring, smem + lay.bars, smem + lay.ctab, warp, lane);
+    ring.init(smem + lay.ring, smem + lay.bars, smem + lay.ctab, warp);
     decltype(ring)::init_barriers(smem + lay.bars, NW, tid);
     gsync();
   }

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kNT, 1)
   const int nitems = items[0];
   Ring ring;
   if constexpr (RING) {
-    ring.init(smem + lay.ring, smem + lay.bars, smem + lay.ctab, warp, lane);
+    ring.init(smem + lay.ring, smem + lay.bars, smem + lay.ctab, warp);
     Ring::init_barriers(smem + lay.bars, kNW, tid);
     __syncthreads();
   }

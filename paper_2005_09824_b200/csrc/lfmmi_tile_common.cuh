@@ -105,6 +105,9 @@ __device__ __forceinline__ uint32_t lds_h(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ void sts_v2(uint32_t a, uint2 v) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
 __device__ __forceinline__ void sts_f(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(a), "f"(v));
 }
