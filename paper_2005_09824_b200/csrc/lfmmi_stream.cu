@@ -232,8 +232,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     if constexpr (RING) {
       ring.rows(trips, body);
     } else {
-#pragma unroll 8
-      for (int j = 0; j < trips; ++j) body(ldg_slot(sp + 32 * j));
+      // 8 slot-row loads in flight per lane before their arc bodies (L2 latency)
+      int j = 0;
+      for (; j + 8 <= trips; j += 8) {
+        uint2 w[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) w[r] = ldg_slot(sp + 32 * (j + r));
+#pragma unroll
+        for (int r = 0; r < 8; ++r) body(w[r]);
+      }
+      for (; j < trips; ++j) body(ldg_slot(sp + 32 * j));
     }
   };
   if constexpr (RING) {

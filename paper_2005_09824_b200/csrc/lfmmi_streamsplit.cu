@@ -5,7 +5,9 @@
 // assignment of the batch: CTA 0 runs the forward recursion over frames
 // 0..T-1, CTA 1 the backward recursion over T-1..0, concurrently, each with
 // the full columns in its own shared memory and the stream packs (32-state
-// tiles, bank-scheduled rows) read from L2.  They meet at h (~T/2):
+// tiles, bank-scheduled rows) streamed from L2 through the per-warp TMA slot
+// ring (lfmmi_ring.cuh) when it fits beside the columns, else read per row from
+// L2.  They meet at h (~T/2):
 //
 //   forward  frames 0..h-1 : alpha, spilled to trellis rows 0..h-1 (backward-pack order)
 //            frames h..T-1 : alpha + posteriors of those frames (using beta' rows)
@@ -235,8 +237,16 @@ __global__ void __launch_bounds__(kNT, 1)
       if constexpr (RING) {
         ring.rows(trips, body);
       } else {
-#pragma unroll 8
-        for (int j = 0; j < trips; ++j) body(ldg_slot(sp + 32 * j));
+        // 8 slot-row loads in flight per lane before their arc bodies (L2 latency)
+        int j = 0;
+        for (; j + 8 <= trips; j += 8) {
+          uint2 w[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) w[r] = ldg_slot(sp + 32 * (j + r));
+#pragma unroll
+          for (int r = 0; r < 8; ++r) body(w[r]);
+        }
+        for (; j < trips; ++j) body(ldg_slot(sp + 32 * j));
       }
     };
     // this CTA's arc-loop frames of the item: forward T (fewer only on a
