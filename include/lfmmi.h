@@ -64,7 +64,8 @@ const char *lfmmi_last_error(void);
  *   tile_xdb, tile_persist den tile kernel: double-buffered slots; persistent CTAs
  *                          over an in-kernel LPT when B > SMs (0 off, 1 auto, >= 2 force)
  *   stream_mode            "auto", "split", "1024x1", "1024x2", "512x2"
- *   stream_ring            TMA slot ring of the stream kernels
+ *   stream_ring            TMA slot ring of the 1024x1 / 1024x2 stream kernels
+ *   ssplit_ring            ... of the stream split kernel (default off)
  *   num_group              threads per utterance of the generic numerator kernel
  *   serial                 -1 auto / 0 / 1: numerator pass before the den pass
  *   sched_iters, chore_bias     pack-time scheduling knobs

@@ -42,9 +42,7 @@ int launch_linear(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st
 
 // Forward | backward split of the L2-streamed kernel (lfmmi_streamsplit.cu):
 // fp32, uniform leak, WRITE / NEGATE; LFMMI_ERR_UNSUPPORTED when not applicable.
-// ring_only: LFMMI_ERR_UNSUPPORTED unless the TMA slot ring fits (auto dispatch).
-int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st,
-                        bool ring_only = false);
+int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st);
 
 // Emissions pre-pass (lfmmi_api.cu emit_kernel): E = exp(L - m), Em = m per valid row.
 int launch_emit(const float *L, const int *lengths, int B, int T_max, int D, bool packed,

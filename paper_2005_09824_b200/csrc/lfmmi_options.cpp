@@ -29,6 +29,7 @@ const Field kFields[] = {
     {"split_h64", &Options::split_h64, nullptr},
     {"stream_mode", nullptr, &Options::stream_mode},
     {"stream_ring", &Options::stream_ring, nullptr},
+    {"ssplit_ring", &Options::ssplit_ring, nullptr},
     {"num_group", &Options::num_group, nullptr},
     {"small_arcs", &Options::small_arcs, nullptr},
     {"small_indeg", &Options::small_indeg, nullptr},

@@ -20,6 +20,7 @@ struct Options {
   int split_clusters = 0; // 0 = auto
   int split_h64 = 33;     // split midpoint in 64ths of T
   std::string stream_mode = "auto";  // "auto" | "1024x1" | "1024x2" | "512x2"
+  int ssplit_ring = 0;   // stream split kernel: TMA slot ring (L2 rows measured faster)
   int stream_ring = 1;    // stream kernel: TMA slot ring when it fits (biphone 9.45 vs 9.96 ms)
   int num_group = 128;    // threads per utterance of the generic (tile) numerator kernel
   int small_arcs = 1024;  // graphs with <= 512 states, <= this many arcs per row AND in-degree

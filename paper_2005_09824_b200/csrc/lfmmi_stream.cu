@@ -534,16 +534,14 @@ int launch_stream<float>(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStre
   // Two SMs per utterance (2-CTA cluster of 1024-thread CTAs) while the batch
   // leaves SMs idle, else one 1024-thread CTA per utterance.  ("512x2" — two
   // half-utterance CTAs per SM — measured slower on biphone: 14.1 vs 12.4 ms.)
-  // "split": the forward | backward split (lfmmi_streamsplit.cu).  With the TMA
-  // slot ring it is the default once the batch fills the SMs (biphone 7.75 vs
-  // 9.09 ms for 1024x1 with its ring); reading slot rows from L2 it is not
-  // faster (biphone 9.67 ms, large 35.5 vs 30.7 ms: frames latency-bound on the
-  // per-warp slot loads), so graphs whose columns leave no room for the ring
-  // (large) stay on 1024x2 / 1024x1.
+  // "split" (the default when it applies): the forward | backward split
+  // (lfmmi_streamsplit.cu), slot rows from L2 with 8 row loads in flight per
+  // lane — biphone 7.09 ms (split + TMA ring 7.68, 1024x1 + ring 8.42), large
+  // 23.6 ms (1024x2 27.1).
   const std::string &want = options().stream_mode;
   if (want == "split") return launch_stream_split(a, g, st);
-  if (want == "auto" && 2 * a.B > sms && options().stream_ring) {
-    const int rc = launch_stream_split(a, g, st, true);
+  if (want == "auto") {
+    const int rc = launch_stream_split(a, g, st);
     if (rc != LFMMI_ERR_UNSUPPORTED) return rc;
   }
   std::string mode = want != "auto" ? want : (2 * a.B <= sms ? "1024x2" : "1024x1");

@@ -541,8 +541,7 @@ __global__ void __launch_bounds__(kNT, 1)
   }
 }
 
-int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st,
-                        bool ring_only) {
+int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStream_t st) {
   if (!g->streamable) return set_error(LFMMI_ERR_UNSUPPORTED, "graph has no stream pack");
   if (a.leak_pi) return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: uniform leak only");
   if (a.D > kMaxD) return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: D > 2048");
@@ -555,9 +554,10 @@ int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   // TMA ring when its table holds a warp's chunks and it fits next to the columns
   const int tiles_per_warp = (g->max_stiles + kNW - 1) / kNW;
   const int max_deg = std::max(g->max_in_deg, g->max_out_deg);
-  bool ring = opt.stream_ring != 0 && ring_chunks_needed(tiles_per_warp, max_deg, 8) <= 64 &&
+  // (option ssplit_ring: the TMA slot ring; off by default since the L2 path
+  // with 8 row loads in flight per lane measured faster: biphone 7.09 vs 7.68 ms)
+  bool ring = opt.ssplit_ring != 0 && ring_chunks_needed(tiles_per_warp, max_deg, 8) <= 64 &&
               ss_layout(S32, a.D_pad, a.T_pad, true).total <= unsigned(kMaxSmem);
-  if (ring_only && !ring) return set_error(LFMMI_ERR_UNSUPPORTED, "stream split: no ring");
   const SSLayout lay = ss_layout(S32, a.D_pad, a.T_pad, ring);
   if (lay.total > unsigned(kMaxSmem))
     return set_error(LFMMI_ERR_UNSUPPORTED,

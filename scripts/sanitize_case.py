@@ -41,8 +41,8 @@ CASES = {
     "stream2": ("wsj_biphone", 2, dict(stream_mode="1024x2")),
     "stream1": ("wsj_biphone", 2, dict(stream_mode="1024x1", stream_ring=0)),
     "ring": ("wsj_biphone", 2, dict(stream_mode="1024x1", stream_ring=1)),
-    "ssplit": ("wsj_biphone", 3, dict(stream_mode="split")),
-    "ssplit0": ("wsj_biphone", 3, dict(stream_mode="split", stream_ring=0)),
+    "ssplit": ("wsj_biphone", 3, dict(stream_mode="split", ssplit_ring=1)),
+    "ssplit0": ("wsj_biphone", 3, dict(stream_mode="split")),
     "hmm": ("hmm", 3, dict()),
     "tilep": ("wsj_mono", 3, dict(split=0, tile_persist=2)),
     "lin16": ("wsj_mono", 2, dict()),

@@ -147,10 +147,10 @@ def _kernel_env(kernel, lib_options):
         lib_options(tile_g=4, split=1)
     if kernel == "tilep":  # den tile kernel as 2 persistent CTAs over the in-kernel LPT
         lib_options(split=0, tile_persist=2)
-    if kernel == "ssplit":  # L2-resident graphs: forward | backward stream split (TMA ring)
+    if kernel == "ssplit":  # L2-resident graphs: forward | backward stream split with its TMA ring
+        lib_options(stream_mode="split", ssplit_ring=1)
+    if kernel == "ssplit0":  # ... slot rows straight from L2 (the default)
         lib_options(stream_mode="split")
-    if kernel == "ssplit0":  # ... slot rows straight from L2
-        lib_options(stream_mode="split", stream_ring=0)
 
 
 @pytest.mark.parametrize("kernel", ["auto", "tile", "split2", "tile1x", "numtile", "noring",
@@ -176,11 +176,14 @@ def test_configs_vs_oracle(cuda, config, batch_size, kernel, lib_options):
 @pytest.mark.parametrize("kernel", ["ssplit", "stream", "stream1", "stream512", "group"])
 def test_large_graph_l2_path_vs_oracle(cuda, kernel, lib_options):
     """Config 4 (20k states / 200k arcs / 2000 pdfs): the arc packs do not fit in
-    shared memory.  "stream": coalesced 32-state tiles streamed from L2
-    (fb_stream_kernel); "group": the generic CSR kernel with alpha read back
-    from the HBM trellis."""
+    shared memory.  "ssplit": the default forward | backward stream split;
+    "stream": coalesced 32-state tiles streamed from L2 by one 2-CTA cluster per
+    utterance (fb_stream_kernel<1024,2>); "group": the generic CSR kernel with
+    alpha read back from the HBM trellis."""
     if kernel == "group":
         lib_options(stream=0)
+    if kernel == "stream":
+        lib_options(stream_mode="1024x2")
     if kernel == "ssplit":  # forward | backward split (fb_streamsplit_kernel)
         lib_options(stream_mode="split")
     if kernel == "stream1":  # one CTA per utterance instead of a 2-CTA cluster
@@ -306,11 +309,14 @@ def test_nan_frame_fails_one_utterance_every_path(cuda, config, batch_size, kern
     assert np.abs(res.grad - ref.grad).max() <= FP32_GRAD_ABS
 
 
-@pytest.mark.parametrize("mode", ["split", "1024x1", "1024x2"])
+@pytest.mark.parametrize("mode", ["split", "splitring", "1024x1", "1024x2"])
 def test_stream_kernel_short_utterances(cuda, mode, lib_options):
     """1-, 2- and 3-frame utterances through the L2-streamed kernel (biphone-sized
     denominator): prologue / epilogue edges of the register row pipeline."""
-    lib_options(stream_mode=mode)
+    if mode == "splitring":
+        lib_options(stream_mode="split", ssplit_ring=1)
+    else:
+        lib_options(stream_mode=mode)
     w = synth.make_workload("wsj_biphone", seed=10, batch_size=4)
     rng = np.random.default_rng(0)
     seqs = [rng.normal(0, 2, (t, w.D)).astype(np.float32).astype(np.float64) for t in (1, 2, 3, 7)]
