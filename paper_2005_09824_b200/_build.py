@@ -23,7 +23,8 @@ INCLUDE = os.path.join(ROOT, "include")
 # Build-time variants for same-box A/B measurements (development only): an
 # extra set of -D flags, built into _lib_<name>/ and selected at import time
 # by LFMMI_LIB_VARIANT=<name>.  The default build is _lib/.
-VARIANTS = {"rows8": ["-DLFMMI_SLOT_ROWS=8"]}
+VARIANTS = {"rows8": ["-DLFMMI_SLOT_ROWS=8"], "l2r12": ["-DLFMMI_L2_ROWS=12"],
+            "l2r16": ["-DLFMMI_L2_ROWS=16"]}
 VARIANT = os.environ.get("LFMMI_LIB_VARIANT", "")
 LIB_DIR = os.path.join(PKG, "_lib" + (f"_{VARIANT}" if VARIANT else ""))
 CORE_SO = os.path.join(LIB_DIR, "libpaper_lfmmi.so")

@@ -54,6 +54,10 @@ constexpr int kNT = 1024, kNW = kNT / 32;
 constexpr int kMaxD = 2048, kEPT = (kMaxD + kNT - 1) / kNT;  // log-likelihood elements per thread
 constexpr float kPostScale = 268435456.f;        // 2^28
 constexpr int kMaxItems = kLptMaxItems;          // utterances per cluster
+#ifndef LFMMI_L2_ROWS
+#define LFMMI_L2_ROWS 8
+#endif
+constexpr int kL2Rows = LFMMI_L2_ROWS;  // slot-row loads in flight per lane (L2 path)
 // TMA slot ring (as fb_stream_kernel): 2 chunks of 8 slot rows per warp
 using Ring = SlotRing<2, 8, 64>;
 
@@ -239,12 +243,12 @@ __global__ void __launch_bounds__(kNT, 1)
       } else {
         // 8 slot-row loads in flight per lane before their arc bodies (L2 latency)
         int j = 0;
-        for (; j + 8 <= trips; j += 8) {
-          uint2 w[8];
+        for (; j + kL2Rows <= trips; j += kL2Rows) {
+          uint2 w[kL2Rows];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) w[r] = ldg_slot(sp + 32 * (j + r));
+          for (int r = 0; r < kL2Rows; ++r) w[r] = ldg_slot(sp + 32 * (j + r));
 #pragma unroll
-          for (int r = 0; r < 8; ++r) body(w[r]);
+          for (int r = 0; r < kL2Rows; ++r) body(w[r]);
         }
         for (; j < trips; ++j) body(ldg_slot(sp + 32 * j));
       }
