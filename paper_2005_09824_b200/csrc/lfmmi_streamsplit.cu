@@ -569,8 +569,9 @@ int launch_stream_split(const FBArgs<float> &a, const lfmmi_graphs *g, cudaStrea
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // every SM pair but two (the numerator pass runs beside this one)
-  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2 - 2);
+  // every SM pair: the numerators (0.85 ms alone at biphone) run in the
+  // denominator's tail (biphone step 7.10 / 7.04 ms with 72 / 74 clusters)
+  int nc = opt.split_clusters > 0 ? opt.split_clusters : std::min(a.B, sms / 2);
   nc = std::max(1, std::min(nc, std::min(96, sms / 2)));
   nc = std::max(nc, (a.B + kMaxItems - 1) / kMaxItems);
   if (nc > std::min(96, sms / 2))
