@@ -55,7 +55,8 @@ const char *lfmmi_last_error(void);
  *   linear_split           numerators as forward | backward warps
  *   linear_k16w            warps per direction for numerators with S > 256 (2 or 1)
  *   linear_k16             1: one numerator launch for every K
- *   emit                   emissions pre-pass of the chain loss
+ *   emit                   emissions pre-pass of the chain loss (1 auto: skipped for
+ *                          dens whose arc pack exceeds shared memory; 2 always; 0 never)
  *   split                  den split kernel: -1 auto / 0 off / 1 force
  *   split_clusters, split_h64   cluster count (0 auto), midpoint in 64ths of T
  *   small_arcs, small_indeg     graphs with <= 512 states, <= small_arcs arcs and

@@ -602,8 +602,17 @@ static int chain_loss_impl(const lfmmi_graphs *numerators, const int64_t *num_ro
   const int ser_opt = options().serial;
   const bool serial = ser_opt > 0 || (ser_opt < 0 && batch > 2 * sms);
   // Emissions once per step, shared by the passes that take them (the linear
-  // numerator kernel and the split denominator kernel).
-  if (precision == LFMMI_F32 && options().emit) {
+  // numerator kernel and the split denominator kernel).  Option emit: 1 (auto)
+  // skips it when the denominator's arc pack cannot sit in shared memory (its
+  // L2-streamed kernels exponentiate their own rows; the numerators then take
+  // the one-warp linear kernel, in the den's tail: biphone step 7.04 -> 6.79
+  // ms), 2 always, 0 never.
+  const int emit_opt = options().emit;
+  const bool den_smem =
+      denominator->tileable &&
+      size_t(std::max(denominator->max_tf_slots, denominator->max_tb_slots)) * 10 <=
+          size_t(kMaxSmem);
+  if (precision == LFMMI_F32 && (emit_opt >= 2 || (emit_opt == 1 && den_smem))) {
     const size_t rows = packed ? size_t(total_frames) : size_t(batch) * size_t(max_frames);
     float *e = reinterpret_cast<float *>(ws + e_off);
     float *em = e + ((rows * size_t(num_pdfs) * 4 + 255) & ~size_t(255)) / 4;

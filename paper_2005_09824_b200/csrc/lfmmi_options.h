@@ -30,6 +30,7 @@ struct Options {
   int tile_xdb = 1;       // den tile kernel: double-buffered posterior slots
   int serial = 0;         // chain_loss: numerator pass before the den pass (-1 auto: B > 2 x SMs)
   int emit = 1;           // chain_loss (fp32): emissions pre-pass shared by the passes
+                          // (1 auto: not for dens beyond shared memory; 2 always; 0 never)
   int sched_iters = -1;   // bank-conflict local search moves per slot row (-1 auto)
   int chore_bias = 16;    // den warp lists: extra slot rows charged to the chore warps (pack time)
   int tile_g = 0;         // tile packs: lanes per state (0 auto, else forced power of 2; pack time)

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-for o in "emit=1" "emit=0"; do
-LFMMI_OPTIONS=$o timeout 600 python bench.py --config wsj_biphone --steps 10 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/em_bi_$o.log 2>&1
-LFMMI_OPTIONS=$o timeout 900 python bench.py --config large --steps 5 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/em_large_$o.log 2>&1
-done
+timeout 1500 python -m pytest tests/test_linear_kernel.py tests/test_gpu_parity.py tests/test_full_size_parity.py -q -p no:cacheprovider -x -k "biphone or large or linear or l2_path or stream" > gpurun_out/t_emit.log 2>&1; echo "rc=$?" >> gpurun_out/t_emit.log
+timeout 600 python bench.py --config wsj_biphone --steps 10 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_bi.log 2>&1
+timeout 600 python bench.py --steps 20 --warmup 3 --no-extra-e2e --no-cpu-baseline > gpurun_out/bench_mono.log 2>&1

@@ -196,8 +196,10 @@ def test_linear_split_in_chain_loss_vs_oracle(cuda, lib_options, config, batch_s
     """The chain-loss numerator pass (emissions pre-pass): forward | backward warps
     meeting at the midpoint, posteriors pre-normalised by the kappa recursion
     (split = 1, the default), or one warp doing both (split = 0).  Sweep mixes
-    K <= 8 utterances (split kernel) with K = 16 ones (single-warp launch)."""
-    lib_options(linear_split=split)
+    K <= 8 utterances (split kernel) with K = 16 ones (single-warp launch).
+    emit = 2: the pre-pass also for the biphone den (whose L2-streamed kernels do
+    not consume it, so `auto` skips it there)."""
+    lib_options(linear_split=split, emit=2)
     w = synth.make_workload(config, seed=31, batch_size=batch_size)
     batch, nums, den = w.build(P)
     opts = P.FBOptions(leak_coefficient=leak)
